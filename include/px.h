@@ -1,0 +1,176 @@
+/*
+ * px.h -- C-ABI of libpx.so, the B200 (sm_100a) implementation of the PERCH 2.0
+ * parallel-search hot path: render -> GICP refine -> re-render -> cost -> argmin.
+ *
+ * The reference (Python package `rvpose`) has no FFI layer; its boundary for this
+ * path is the Python API re-exported in pkg/src/rvpose/__init__.py:9-66.  Each
+ * entry point below names the reference function it replaces (paths relative to
+ * /root/reference/pkg/src/rvpose/).  INTEGRATION.md shows the ctypes binding a
+ * maintainer of the reference would add.
+ *
+ * Conventions: plain pointers and sizes only; every array is C-contiguous;
+ * float64 / int32 / uint8 as stated; the caller owns all host buffers, the
+ * context owns all device memory; one context per device, not thread-safe; every
+ * call is synchronous at return (inputs consumed, outputs written) unless noted.
+ * Return value 0 = success, negative = error (PX_E_*); the message is available
+ * from px_last_error().  There is no CPU fallback: without a CUDA device
+ * px_ctx_create fails.
+ */
+#ifndef PX_H_
+#define PX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PX_E_CUDA (-1)      /* CUDA runtime error */
+#define PX_E_ARG (-2)       /* bad argument / unknown object id / state missing */
+#define PX_E_LIMIT (-3)     /* implementation limit exceeded (see message) */
+
+/* failure codes in the low byte of `flags` (registration.py:434-456, 504-510);
+ * bit 8 (0x100) = converged */
+#define PX_FAIL_NONE 0
+#define PX_FAIL_TOO_FEW_POINTS 1
+#define PX_FAIL_DEGENERATE_CORRESPONDENCES 2
+#define PX_FAIL_SINGULAR_NORMAL_EQUATIONS 3
+#define PX_FAIL_NO_DECREASE 4
+#define PX_FLAG_CONVERGED 0x100
+
+typedef struct px_ctx px_ctx;
+typedef struct px_clouds px_clouds; /* device-resident ragged batch of LabeledCloud (model.py:185-217) */
+
+/* GicpConfig, registration.py:26-42 */
+typedef struct {
+  int32_t k_covariance;
+  int32_t max_iterations;
+  double epsilon;
+  double translation_tolerance;
+  double rotation_tolerance;
+  double max_correspondence_distance;
+} px_gicp_cfg;
+
+/* The part of SearchConfig (search.py:37-61) the per-candidate stages read, plus
+ * the camera extrinsics used by the 3-DoF re-lift (search.py:295-299). */
+typedef struct {
+  int32_t mode3dof;          /* 1 = "3dof" (cylinder association, planar re-lift), 0 = "6dof" (labels) */
+  int32_t use_color;
+  int32_t occluder_marking;
+  int32_t refine;
+  double delta;              /* also delta_occ, search.py:276 */
+  double tau_c;
+  px_gicp_cfg gicp;
+  double cam_to_world[12];   /* row-major 3x4 */
+  double world_to_cam[12];
+  int32_t c2w_vec_order;     /* 0: host rotation array is C-contiguous, 1: transposed view */
+  int32_t w2c_vec_order;     /*    (selects numpy's (3,3)@(3,) rounding order) */
+  double fixed_z;
+} px_search_cfg;
+
+/* ---- context ---------------------------------------------------------------- */
+int px_ctx_create(int device, px_ctx** out);
+void px_ctx_destroy(px_ctx* ctx);
+const char* px_last_error(const px_ctx* ctx); /* ctx may be NULL: last creation error */
+/* Launch on a caller-provided cudaStream_t (e.g. torch's current stream); NULL
+ * restores the context's own stream. */
+int px_ctx_set_stream(px_ctx* ctx, void* cuda_stream);
+int px_ctx_sync(px_ctx* ctx);
+/* Upper bound in bytes for per-chunk candidate scratch (default 8 GiB). */
+int px_ctx_set_scratch_budget(px_ctx* ctx, int64_t bytes);
+/* Kernels launched by this context since creation (bench.py's gpu_launches). */
+int64_t px_ctx_launch_count(const px_ctx* ctx);
+
+/* ---- per-scene / per-model state -------------------------------------------- */
+/* SceneFrame planes + the observed cloud of raster.frame_to_cloud / cloud_labels
+ * (raster.py:191-217), computed by the caller.  obs_src_px is (n_obs,2) (u,v).
+ * If the cloud is the stride-grid cloud of this frame it is indexed as an
+ * organised grid (fast path); otherwise px_search / px_cost_batch refuse it and
+ * px_rendered_cost (brute force) is the path to use. */
+int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
+                    const int32_t* labels, const double intr[4] /* fx fy cx cy */, int32_t stride,
+                    const double* obs_points, const double* obs_lab, const int32_t* obs_src_px,
+                    const int32_t* obs_labels, int64_t n_obs);
+/* ObjectModel (model.py:75-85): mesh with colours already decoded to linear light
+ * (colorspace.srgb_decode, done once per model on the host), inscribed cylinder
+ * as (radius**2, z_min, z_max).  Re-uploading an id replaces it. */
+int px_model_upload(px_ctx* ctx, int32_t object_id, const double* verts, const double* colors_linear,
+                    const int32_t* tris, int64_t V, int64_t T, const double cyl[3]);
+
+/* ---- raster.render_batch (raster.py:283-304) -------------------------------- */
+int px_render_batch(px_ctx* ctx, const int32_t* object_ids, const double* poses3x4, int64_t n,
+                    int32_t occluder_marking, double delta_occ, px_clouds** out);
+int64_t px_clouds_count(const px_clouds* c);
+/* counts (n) int32 */
+int px_clouds_counts(px_ctx* ctx, const px_clouds* c, int32_t* counts);
+/* compacted copies, sum(counts) rows each; any pointer may be NULL */
+int px_clouds_download(px_ctx* ctx, const px_clouds* c, double* points, double* lab, int32_t* src_px);
+/* caller-provided clouds (for m2m_gicp / cost on arbitrary LabeledClouds) */
+int px_clouds_upload(px_ctx* ctx, int64_t n, const int32_t* counts, const double* points,
+                     const double* lab /* nullable */, const int32_t* src_px /* nullable */, px_clouds** out);
+void px_clouds_free(px_ctx* ctx, px_clouds* c);
+
+/* raster.rasterize (raster.py:137-158) without the final sRGB encode: full-image
+ * z-buffer (inf = empty), linear colour, validity and owning triangle (-1). */
+int px_rasterize(px_ctx* ctx, int32_t object_id, const double pose3x4[12], double* zbuf, double* cbuf_linear,
+                 uint8_t* valid, int32_t* owner);
+
+/* ---- registration (registration.py:219-230, 514-550) ------------------------ */
+/* estimate_covariances for one cloud; n must exceed k (else PX_E_ARG). */
+int px_covariances(px_ctx* ctx, const double* points, int64_t n, int32_t k, double epsilon, double* cov_out);
+/* Target clouds of m2m_gicp: offsets (n_targets+1), points (offsets[n],3).
+ * Covariances are built once per distinct target on the device. */
+int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, const double* points,
+                      int32_t k_covariance, double epsilon);
+int px_targets_covariances(px_ctx* ctx, double* cov_out); /* (offsets[n],9), for tests */
+/* m2m_gicp: one source cloud per entry, target_idx into the uploaded targets,
+ * init_T (n,12) or NULL = identity.  Outputs (any may be NULL): out_T (n,12)
+ * [orthonormalised R | t], iterations, flags, rms residual, objective trace
+ * (n, max_iterations, 2) with n_trace accepted steps per entry. */
+int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target_idx, const double* init_T,
+                    const px_gicp_cfg* cfg, double* out_T, int32_t* out_iters, int32_t* out_flags,
+                    double* out_residual, double* out_trace, int32_t* out_ntrace);
+
+/* ---- cost (cost.py:91-162, search.py:189-202) -------------------------------- */
+/* Per-candidate (j_o, j_r) against the uploaded organised scene.  cyl_poses
+ * (n,12) = camera-frame object pose per candidate for the inscribed-cylinder
+ * association, or NULL for the pixel-label association. */
+int px_cost_batch(px_ctx* ctx, const px_clouds* rendered, const int32_t* object_ids, const double* cyl_poses,
+                  double delta, double tau_c, int32_t use_color, int32_t* j_o, int32_t* j_r);
+/* cost.rendered_cost on arbitrary clouds (brute-force exact NN, neighbors.py
+ * semantics): returns j_r and the explained mask (n_obs bytes). */
+int px_rendered_cost(px_ctx* ctx, const double* ren_points, const double* ren_lab, int64_t n_r,
+                     const double* obs_points, const double* obs_lab, int64_t n_obs, double delta,
+                     double tau_c, int32_t use_color, int32_t* j_r, uint8_t* explained);
+/* neighbors.knn_full / knn_streamed: exact k nearest, ties -> lowest index;
+ * idx (nq,k) int64 (-1 = missing), d2 (nq,k) (+inf = missing); k <= 32. */
+int px_knn(px_ctx* ctx, const double* queries, int64_t nq, const double* targets, int64_t nt, int32_t k,
+           int64_t* idx, double* d2);
+
+/* ---- the fused search driver (search.py:268-372 for the flat candidate list) - */
+/* Candidate-resident inputs.  object_ids / poses3x4 / rank_in_object are (n);
+ * target_idx (n) may be NULL when cfg.refine == 0.  rank_in_object is the
+ * candidate's position among its object's candidates (select_best's index). */
+int px_search_upload(px_ctx* ctx, int64_t n, const int32_t* object_ids, const double* poses3x4,
+                     const int32_t* target_idx, const int32_t* rank_in_object);
+/* Run render -> refine -> re-render -> cost -> per-object argmin on the resident
+ * candidates; results stay on the device.  Asynchronous only in the sense that
+ * stage timing uses CUDA events on the context stream; returns after the last
+ * kernel has been enqueued and chunk sizing has synchronised as needed. */
+int px_search_run(px_ctx* ctx, const px_search_cfg* cfg);
+/* Copy results to the host (any pointer may be NULL): refined candidate poses
+ * (n,12), applied GICP corrections (n,12), iterations, flags, j_o, j_r, points in
+ * the first / final render, packed argmin keys per uploaded model in upload
+ * order ((j_o+j_r) << 32 | rank, UINT64_MAX if the model had no candidate), and
+ * stage milliseconds {render, refine, rerender, cost}. */
+int px_search_download(px_ctx* ctx, double* refined_poses, double* reg_T, int32_t* iters, int32_t* flags,
+                       int32_t* j_o, int32_t* j_r, int32_t* n_first, int32_t* n_final,
+                       uint64_t* best_key_per_model, double stage_ms[4]);
+/* Number of models uploaded and their ids in slot order (for best_key_per_model). */
+int px_model_count(const px_ctx* ctx);
+int px_model_ids(const px_ctx* ctx, int32_t* ids);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PX_H_ */

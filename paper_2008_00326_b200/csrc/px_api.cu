@@ -1,0 +1,965 @@
+// px_api.cu -- context, device memory and the C-ABI of libpx.so (include/px.h).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/px.h"
+#include "px_kernels.h"
+
+using namespace px;
+
+namespace {
+
+std::string g_create_error;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr, cap = 0;
+    size_t want = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr, cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct ModelHost {
+  int32_t object_id;
+  int V, T;
+  double cyl[3];
+  DevBuf verts, col, tris;
+};
+
+struct CloudStore {  // ragged per-candidate clouds with capacity slots
+  int64_t n = 0;
+  long long total_cap = 0;
+  DevBuf bbox, cap, offset, count, points, lab, src;
+  void release() { bbox.release(), cap.release(), offset.release(), count.release(), points.release(), lab.release(), src.release(); }
+};
+
+}  // namespace
+
+struct px_clouds {
+  CloudStore s;
+};
+
+struct px_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr, own_stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int64_t scratch_budget = (int64_t)8 << 30;
+  // scene
+  bool have_scene = false, organised = false;
+  Camera cam{};
+  int64_t n_obs = 0;
+  DevBuf depth, valid, labels, obs_pts, obs_lab, obs_labels, gx, gy, gz, gidx;
+  std::vector<int32_t> h_obs_labels;
+  // models
+  std::vector<ModelHost*> models;
+  std::map<int32_t, int> slot_of;
+  DevBuf models_dev, label_count;
+  bool models_dirty = true;
+  size_t render_smem = 0;
+  // targets
+  int n_targets = 0;
+  long long tgt_total = 0;
+  int tgt_k = 0;
+  DevBuf tgt_off, tgt_pts, tgt_cov;
+  // resident candidates
+  int64_t n_cand = 0;
+  bool have_tidx = false;
+  DevBuf c_slot, c_pose, c_tidx, c_rank;
+  // search scratch / results
+  CloudStore clouds;
+  DevBuf src_cov, w_buf, corr, total_dev;
+  DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap;
+  int bitmap_slots = 0;
+  long long* total_host = nullptr;  // pinned
+  double stage_ms[4] = {0, 0, 0, 0};
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+int fail(px_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_create_error = msg;
+  return code;
+}
+#define CU(call)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess)                                                                            \
+      return fail(ctx, PX_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));                \
+  } while (0)
+
+int h2d(px_ctx* ctx, DevBuf& b, const void* src, size_t bytes) {
+  CU(b.ensure(bytes ? bytes : 8));
+  if (bytes) CU(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return 0;
+}
+int d2h(px_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes && dst) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return 0;
+}
+
+int sync_models(px_ctx* ctx) {
+  if (!ctx->models_dirty) return 0;
+  std::vector<ModelDev> md(ctx->models.size());
+  std::vector<int32_t> lc(ctx->models.size(), 0);
+  size_t smem = 0;
+  for (size_t i = 0; i < ctx->models.size(); ++i) {
+    ModelHost* m = ctx->models[i];
+    md[i].verts = m->verts.as<double>();
+    md[i].col = m->col.as<double>();
+    md[i].tris = m->tris.as<int32_t>();
+    md[i].V = m->V, md[i].T = m->T, md[i].object_id = m->object_id, md[i].pad_ = 0;
+    md[i].cyl_r2 = m->cyl[0], md[i].cyl_zmin = m->cyl[1], md[i].cyl_zmax = m->cyl[2];
+    md[i].aabb_r = std::sqrt(m->cyl[0]) * (1.0 + 1e-9);
+    smem = std::max(smem, render_smem_bytes(m->V, m->T));
+    for (int32_t l : ctx->h_obs_labels) lc[i] += (l == m->object_id);
+  }
+  ctx->render_smem = smem;
+  if (int r = h2d(ctx, ctx->models_dev, md.data(), md.size() * sizeof(ModelDev))) return r;
+  if (int r = h2d(ctx, ctx->label_count, lc.data(), lc.size() * sizeof(int32_t))) return r;
+  CU(cudaStreamSynchronize(ctx->stream));  // md / lc are stack-owned
+  ctx->models_dirty = false;
+  return 0;
+}
+
+int slots_from_ids(px_ctx* ctx, const int32_t* ids, int64_t n, std::vector<int32_t>& out) {
+  out.resize((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    auto it = ctx->slot_of.find(ids[i]);
+    if (it == ctx->slot_of.end()) return fail(ctx, PX_E_ARG, "no model registered for id " + std::to_string(ids[i]));
+    out[(size_t)i] = it->second;
+  }
+  return 0;
+}
+
+RenderArgs base_render_args(px_ctx* ctx) {
+  RenderArgs a{};
+  a.cam = ctx->cam;
+  a.models = ctx->models_dev.as<ModelDev>();
+  a.obs_depth = ctx->depth.as<double>();
+  a.obs_valid = ctx->valid.as<uint8_t>();
+  a.obs_labels = ctx->labels.as<int32_t>();
+  return a;
+}
+
+// bbox + capacity scan for `n` candidates; returns total capacity via *total
+int size_clouds(px_ctx* ctx, CloudStore& cs, const int32_t* slot_dev, const double* pose_dev, int64_t n,
+                long long* total) {
+  cs.n = n;
+  CU(cs.bbox.ensure(sizeof(int4) * (size_t)n));
+  CU(cs.cap.ensure(sizeof(long long) * (size_t)n));
+  CU(cs.offset.ensure(sizeof(long long) * (size_t)n));
+  CU(cs.count.ensure(sizeof(int32_t) * (size_t)n));
+  RenderArgs a = base_render_args(ctx);
+  a.model_slot = slot_dev, a.poses = pose_dev, a.n = (int)n;
+  a.bbox = cs.bbox.as<int4>(), a.cap = cs.cap.as<long long>();
+  CU(launch_bbox(a, ctx->stream));
+  CU(launch_scan(cs.cap.as<long long>(), cs.offset.as<long long>(), ctx->total_dev.as<long long>(), (int)n, ctx->stream));
+  ctx->launches += 2;
+  CU(cudaMemcpyAsync(ctx->total_host, ctx->total_dev.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *total = *ctx->total_host;
+  cs.total_cap = *total;
+  return 0;
+}
+
+int render_clouds(px_ctx* ctx, CloudStore& cs, const int32_t* slot_dev, const double* pose_dev, int64_t n,
+                  int occl, double delta_occ) {
+  size_t tot = (size_t)std::max<long long>(cs.total_cap, 1);
+  CU(cs.points.ensure(sizeof(double) * 3 * tot));
+  CU(cs.lab.ensure(sizeof(double) * 3 * tot));
+  CU(cs.src.ensure(sizeof(int32_t) * 2 * tot));
+  RenderArgs a = base_render_args(ctx);
+  a.model_slot = slot_dev, a.poses = pose_dev, a.n = (int)n;
+  a.occluder_marking = occl, a.delta_occ = delta_occ;
+  a.bbox = cs.bbox.as<int4>(), a.cap = cs.cap.as<long long>(), a.offset = cs.offset.as<long long>();
+  a.count = cs.count.as<int32_t>();
+  a.points = cs.points.as<double>(), a.lab = cs.lab.as<double>(), a.src_px = cs.src.as<int32_t>();
+  CU(launch_render(a, ctx->render_smem, false, ctx->stream));
+  ctx->launches += 1;
+  return 0;
+}
+
+CloudsDev clouds_dev(const CloudStore& cs) {
+  CloudsDev d{};
+  d.n = (int)cs.n;
+  d.offset = cs.offset.as<long long>();
+  d.count = cs.count.as<int32_t>();
+  d.points = cs.points.as<double>();
+  d.lab = cs.lab.as<double>();
+  d.src_px = cs.src.as<int32_t>();
+  return d;
+}
+
+int ensure_bitmap(px_ctx* ctx) {
+  const int words = (ctx->cam.GW * ctx->cam.GH + 31) / 32 + 1;
+  const int slots = 148 * 8 * PX_COST_WARPS;
+  const size_t bytes = sizeof(uint32_t) * (size_t)words * slots;
+  if (ctx->bitmap.cap < bytes || ctx->bitmap_slots != slots) {
+    CU(ctx->bitmap.ensure(bytes));
+    CU(cudaMemsetAsync(ctx->bitmap.p, 0, ctx->bitmap.cap, ctx->stream));
+    ctx->bitmap_slots = slots;
+  }
+  return 0;
+}
+
+int run_cost(px_ctx* ctx, const CloudStore& cs, const int32_t* slot_dev, const double* cyl_pose_dev, double delta,
+             double tau_c, int use_color, int32_t* jo_dev, int32_t* jr_dev, const int32_t* rank_dev,
+             unsigned long long* key_dev) {
+  if (!ctx->organised) return fail(ctx, PX_E_ARG, "scene cloud is not the organised stride-grid cloud");
+  if (int r = ensure_bitmap(ctx)) return r;
+  CostArgs a{};
+  a.ren = clouds_dev(cs);
+  a.cam = ctx->cam;
+  a.models = ctx->models_dev.as<ModelDev>();
+  a.model_slot = slot_dev;
+  a.cyl_poses = cyl_pose_dev;
+  a.gx = ctx->gx.as<double>(), a.gy = ctx->gy.as<double>(), a.gz = ctx->gz.as<double>();
+  a.gidx = ctx->gidx.as<int32_t>();
+  a.obs_lab = ctx->obs_lab.as<double>();
+  a.obs_labels = ctx->obs_labels.as<int32_t>();
+  a.label_count = ctx->label_count.as<int32_t>();
+  a.delta = delta, a.delta2 = delta * delta, a.tau_c = tau_c, a.use_color = use_color;
+  a.bitmap = ctx->bitmap.as<uint32_t>();
+  a.bitmap_words = (ctx->cam.GW * ctx->cam.GH + 31) / 32 + 1;
+  a.bitmap_slots = ctx->bitmap_slots;
+  a.j_o = jo_dev, a.j_r = jr_dev, a.rank = rank_dev, a.best_key = key_dev;
+  CU(launch_cost(a, ctx->stream));
+  ctx->launches += 1;
+  return 0;
+}
+
+GicpCfgDev gicp_dev(const px_gicp_cfg& g) {
+  GicpCfgDev d{};
+  d.k_cov = g.k_covariance, d.max_iter = g.max_iterations, d.eps = g.epsilon;
+  d.tol_t2 = g.translation_tolerance * g.translation_tolerance;
+  d.tol_r2 = g.rotation_tolerance * g.rotation_tolerance;
+  d.gate2 = g.max_correspondence_distance * g.max_correspondence_distance;
+  return d;
+}
+
+int check_gicp(px_ctx* ctx, const px_gicp_cfg& g) {
+  if (g.k_covariance < 4 || g.k_covariance > PX_KCOV_MAX)
+    return fail(ctx, PX_E_LIMIT, "k_covariance must lie in [4, " + std::to_string(PX_KCOV_MAX) + "]");
+  if (g.max_iterations < 0) return fail(ctx, PX_E_ARG, "max_iterations < 0");
+  if (ctx->tgt_k != g.k_covariance) return fail(ctx, PX_E_ARG, "targets were uploaded with a different k_covariance");
+  return 0;
+}
+
+int ensure_refine_scratch(px_ctx* ctx, long long total_cap) {
+  size_t tot = (size_t)std::max<long long>(total_cap, 1);
+  CU(ctx->src_cov.ensure(sizeof(double) * 9 * tot));
+  CU(ctx->w_buf.ensure(sizeof(double) * 9 * tot));
+  CU(ctx->corr.ensure(sizeof(int32_t) * tot));
+  return 0;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int px_ctx_create(int device, px_ctx** out) {
+  px_ctx* ctx = nullptr;
+  if (!out) return fail(nullptr, PX_E_ARG, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(nullptr, PX_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e) +
+                                        " (libpx has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(nullptr, PX_E_ARG, "device index out of range");
+  if ((e = cudaSetDevice(device)) != cudaSuccess) return fail(nullptr, PX_E_CUDA, cudaGetErrorString(e));
+  ctx = new px_ctx();
+  ctx->device = device;
+  if ((e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, PX_E_CUDA, cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own_stream;
+  cudaMallocHost((void**)&ctx->total_host, sizeof(long long));
+  ctx->total_dev.ensure(sizeof(long long));
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  *out = ctx;
+  return 0;
+}
+
+void px_ctx_destroy(px_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (ModelHost* m : ctx->models) {
+    m->verts.release(), m->col.release(), m->tris.release();
+    delete m;
+  }
+  DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
+                    &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
+                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
+                    &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->total_dev, &ctx->r_T,
+                    &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
+                    &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap};
+  for (DevBuf* b : bufs) b->release();
+  ctx->clouds.release();
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->total_host) cudaFreeHost(ctx->total_host);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* px_last_error(const px_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+int px_ctx_set_stream(px_ctx* ctx, void* s) {
+  if (!ctx) return PX_E_ARG;
+  cudaStreamSynchronize(ctx->stream);
+  ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
+  return 0;
+}
+
+int px_ctx_sync(px_ctx* ctx) {
+  if (!ctx) return PX_E_ARG;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int px_ctx_set_scratch_budget(px_ctx* ctx, int64_t bytes) {
+  if (!ctx || bytes < (1 << 20)) return fail(ctx, PX_E_ARG, "scratch budget too small");
+  ctx->scratch_budget = bytes;
+  return 0;
+}
+
+int64_t px_ctx_launch_count(const px_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
+                    const int32_t* labels, const double intr[4], int32_t stride, const double* obs_points,
+                    const double* obs_lab, const int32_t* obs_src_px, const int32_t* obs_labels, int64_t n_obs) {
+  if (!ctx) return PX_E_ARG;
+  if (H <= 0 || W <= 0 || stride < 1 || !depth || !valid || !labels || !intr || n_obs < 0)
+    return fail(ctx, PX_E_ARG, "px_scene_upload: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  Camera& c = ctx->cam;
+  c.fx = intr[0], c.fy = intr[1], c.cx = intr[2], c.cy = intr[3];
+  c.W = W, c.H = H, c.stride = stride;
+  c.GW = (W + stride - 1) / stride, c.GH = (H + stride - 1) / stride;
+  const size_t npix = (size_t)H * W;
+  if (int r = h2d(ctx, ctx->depth, depth, npix * sizeof(double))) return r;
+  if (int r = h2d(ctx, ctx->valid, valid, npix)) return r;
+  if (int r = h2d(ctx, ctx->labels, labels, npix * sizeof(int32_t))) return r;
+  if (int r = h2d(ctx, ctx->obs_pts, obs_points, (size_t)n_obs * 24)) return r;
+  if (int r = h2d(ctx, ctx->obs_lab, obs_lab, (size_t)n_obs * 24)) return r;
+  if (int r = h2d(ctx, ctx->obs_labels, obs_labels, (size_t)n_obs * 4)) return r;
+  ctx->n_obs = n_obs;
+  ctx->h_obs_labels.assign(obs_labels, obs_labels + n_obs);
+  // organised-grid view: valid iff every source pixel sits on the stride grid in
+  // strictly increasing row-major order (what raster.frame_to_cloud produces)
+  const size_t ng = (size_t)c.GW * c.GH;
+  std::vector<double> gx(ng, NAN), gy(ng, NAN), gz(ng, NAN);
+  std::vector<int32_t> gi(ng, -1);
+  bool org = obs_src_px != nullptr;
+  long long prev = -1;
+  for (int64_t i = 0; org && i < n_obs; ++i) {
+    const int u = obs_src_px[2 * i], v = obs_src_px[2 * i + 1];
+    if (u < 0 || v < 0 || u >= W || v >= H || u % stride || v % stride) {
+      org = false;
+      break;
+    }
+    const long long g = (long long)(v / stride) * c.GW + u / stride;
+    if (g <= prev) {
+      org = false;
+      break;
+    }
+    prev = g;
+    gx[(size_t)g] = obs_points[3 * i], gy[(size_t)g] = obs_points[3 * i + 1], gz[(size_t)g] = obs_points[3 * i + 2];
+    gi[(size_t)g] = (int32_t)i;
+  }
+  ctx->organised = org;
+  if (org) {
+    if (int r = h2d(ctx, ctx->gx, gx.data(), ng * 8)) return r;
+    if (int r = h2d(ctx, ctx->gy, gy.data(), ng * 8)) return r;
+    if (int r = h2d(ctx, ctx->gz, gz.data(), ng * 8)) return r;
+    if (int r = h2d(ctx, ctx->gidx, gi.data(), ng * 4)) return r;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->have_scene = true;
+  ctx->models_dirty = true;  // label counts depend on the scene
+  ctx->bitmap_slots = 0;     // grid size may have changed
+  return 0;
+}
+
+int px_model_upload(px_ctx* ctx, int32_t object_id, const double* verts, const double* colors_linear,
+                    const int32_t* tris, int64_t V, int64_t T, const double cyl[3]) {
+  if (!ctx) return PX_E_ARG;
+  if (!verts || !colors_linear || V < 3 || T < 0 || (T && !tris) || !cyl)
+    return fail(ctx, PX_E_ARG, "px_model_upload: bad arguments");
+  if (T == 0) return fail(ctx, PX_E_ARG, "mesh has no triangles");
+  for (int64_t i = 0; i < 3 * T; ++i)
+    if (tris[i] < 0 || tris[i] >= V) return fail(ctx, PX_E_ARG, "triangle index out of range");
+  if (render_smem_bytes((int)V, (int)T) > 220 * 1024)
+    return fail(ctx, PX_E_LIMIT, "mesh too large for the shared-memory vertex cache (V <= ~7000)");
+  CU(cudaSetDevice(ctx->device));
+  ModelHost* m;
+  auto it = ctx->slot_of.find(object_id);
+  if (it == ctx->slot_of.end()) {
+    m = new ModelHost();
+    ctx->slot_of[object_id] = (int)ctx->models.size();
+    ctx->models.push_back(m);
+  } else {
+    m = ctx->models[it->second];
+  }
+  m->object_id = object_id, m->V = (int)V, m->T = (int)T;
+  m->cyl[0] = cyl[0], m->cyl[1] = cyl[1], m->cyl[2] = cyl[2];
+  if (int r = h2d(ctx, m->verts, verts, (size_t)V * 24)) return r;
+  if (int r = h2d(ctx, m->col, colors_linear, (size_t)V * 24)) return r;
+  if (int r = h2d(ctx, m->tris, tris, (size_t)T * 12)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->models_dirty = true;
+  return 0;
+}
+
+int px_model_count(const px_ctx* ctx) { return ctx ? (int)ctx->models.size() : 0; }
+int px_model_ids(const px_ctx* ctx, int32_t* ids) {
+  if (!ctx || !ids) return PX_E_ARG;
+  for (size_t i = 0; i < ctx->models.size(); ++i) ids[i] = ctx->models[i]->object_id;
+  return 0;
+}
+
+// ---- render_batch ----------------------------------------------------------
+
+int px_render_batch(px_ctx* ctx, const int32_t* object_ids, const double* poses, int64_t n, int32_t occl,
+                    double delta_occ, px_clouds** out) {
+  if (!ctx || !out || n < 0 || (n && (!object_ids || !poses))) return fail(ctx, PX_E_ARG, "px_render_batch: bad arguments");
+  if (!ctx->have_scene) return fail(ctx, PX_E_ARG, "no scene uploaded");
+  if (n > 0x7fffffff) return fail(ctx, PX_E_LIMIT, "more than 2^31 candidates in one call");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<int32_t> slots;
+  if (int r = slots_from_ids(ctx, object_ids, n, slots)) return r;
+  if (int r = sync_models(ctx)) return r;
+  px_clouds* c = new px_clouds();
+  DevBuf dslot, dpose;
+  int rc = 0;
+  do {
+    if ((rc = h2d(ctx, dslot, slots.data(), (size_t)n * 4))) break;
+    if ((rc = h2d(ctx, dpose, poses, (size_t)n * 96))) break;
+    c->s.n = n;
+    if (n) {
+      long long total = 0;
+      if ((rc = size_clouds(ctx, c->s, dslot.as<int32_t>(), dpose.as<double>(), n, &total))) break;
+      if ((rc = render_clouds(ctx, c->s, dslot.as<int32_t>(), dpose.as<double>(), n, occl, delta_occ))) break;
+    }
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("render: ") + cudaGetErrorString(e));
+  } while (0);
+  dslot.release(), dpose.release();
+  if (rc) {
+    c->s.release();
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return 0;
+}
+
+int64_t px_clouds_count(const px_clouds* c) { return c ? c->s.n : 0; }
+
+int px_clouds_counts(px_ctx* ctx, const px_clouds* c, int32_t* counts) {
+  if (!ctx || !c || !counts) return fail(ctx, PX_E_ARG, "px_clouds_counts: bad arguments");
+  if (int r = d2h(ctx, counts, c->s.count.p, (size_t)c->s.n * 4)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int px_clouds_download(px_ctx* ctx, const px_clouds* c, double* points, double* lab, int32_t* src_px) {
+  if (!ctx || !c) return fail(ctx, PX_E_ARG, "px_clouds_download: bad arguments");
+  const int64_t n = c->s.n;
+  if (n == 0) return 0;
+  std::vector<int32_t> cnt((size_t)n);
+  std::vector<long long> off((size_t)n);
+  if (int r = d2h(ctx, cnt.data(), c->s.count.p, (size_t)n * 4)) return r;
+  if (int r = d2h(ctx, off.data(), c->s.offset.p, (size_t)n * 8)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  // coalesce runs of candidates into few copies: slots are contiguous only when count == cap,
+  // so stage the capacity-strided buffers on the host and compact there
+  const size_t tot = (size_t)std::max<long long>(c->s.total_cap, 0);
+  std::vector<double> hp, hl;
+  std::vector<int32_t> hs;
+  if (points) hp.resize(3 * tot);
+  if (lab) hl.resize(3 * tot);
+  if (src_px) hs.resize(2 * tot);
+  if (int r = d2h(ctx, points ? hp.data() : nullptr, c->s.points.p, 24 * tot)) return r;
+  if (int r = d2h(ctx, lab ? hl.data() : nullptr, c->s.lab.p, 24 * tot)) return r;
+  if (int r = d2h(ctx, src_px ? hs.data() : nullptr, c->s.src.p, 8 * tot)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  size_t w = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const size_t k = (size_t)cnt[(size_t)i], o = (size_t)off[(size_t)i];
+    if (points) memcpy(points + 3 * w, hp.data() + 3 * o, 24 * k);
+    if (lab) memcpy(lab + 3 * w, hl.data() + 3 * o, 24 * k);
+    if (src_px) memcpy(src_px + 2 * w, hs.data() + 2 * o, 8 * k);
+    w += k;
+  }
+  return 0;
+}
+
+int px_clouds_upload(px_ctx* ctx, int64_t n, const int32_t* counts, const double* points, const double* lab,
+                     const int32_t* src_px, px_clouds** out) {
+  if (!ctx || !out || n < 0 || (n && !counts)) return fail(ctx, PX_E_ARG, "px_clouds_upload: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<long long> off((size_t)n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    if (counts[i] < 0) return fail(ctx, PX_E_ARG, "negative cloud size");
+    off[(size_t)i + 1] = off[(size_t)i] + counts[i];
+  }
+  const size_t tot = (size_t)off[(size_t)n];
+  if (tot && !points) return fail(ctx, PX_E_ARG, "points is NULL");
+  px_clouds* c = new px_clouds();
+  c->s.n = n, c->s.total_cap = (long long)tot;
+  int rc = 0;
+  do {
+    if ((rc = h2d(ctx, c->s.offset, off.data(), (size_t)n * 8))) break;
+    if ((rc = h2d(ctx, c->s.count, counts, (size_t)n * 4))) break;
+    if ((rc = h2d(ctx, c->s.points, points, tot * 24))) break;
+    std::vector<double> zl;
+    std::vector<int32_t> zs;
+    if (!lab) zl.assign(3 * tot + 1, 0.0);
+    if (!src_px) zs.assign(2 * tot + 1, 0);
+    if ((rc = h2d(ctx, c->s.lab, lab ? lab : zl.data(), tot * 24))) break;
+    if ((rc = h2d(ctx, c->s.src, src_px ? src_px : zs.data(), tot * 8))) break;
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+  } while (0);
+  if (rc) {
+    c->s.release();
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return 0;
+}
+
+void px_clouds_free(px_ctx* ctx, px_clouds* c) {
+  if (!c) return;
+  if (ctx) cudaStreamSynchronize(ctx->stream);
+  c->s.release();
+  delete c;
+}
+
+int px_rasterize(px_ctx* ctx, int32_t object_id, const double pose[12], double* zbuf, double* cbuf, uint8_t* valid,
+                 int32_t* owner) {
+  if (!ctx || !pose || !zbuf || !cbuf || !valid || !owner) return fail(ctx, PX_E_ARG, "px_rasterize: bad arguments");
+  if (!ctx->have_scene) return fail(ctx, PX_E_ARG, "no scene uploaded (camera comes from the scene)");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<int32_t> slots;
+  if (int r = slots_from_ids(ctx, &object_id, 1, slots)) return r;
+  if (int r = sync_models(ctx)) return r;
+  const size_t npix = (size_t)ctx->cam.W * ctx->cam.H;
+  DevBuf dz, dc, dv, dow, dslot, dpose, dbb, dcap;
+  int rc = 0;
+  do {
+    cudaError_t e;
+    if ((e = dz.ensure(npix * 8)) || (e = dc.ensure(npix * 24)) || (e = dv.ensure(npix)) || (e = dow.ensure(npix * 4)) ||
+        (e = dbb.ensure(sizeof(int4))) || (e = dcap.ensure(8))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    if ((rc = h2d(ctx, dslot, slots.data(), 4))) break;
+    if ((rc = h2d(ctx, dpose, pose, 96))) break;
+    RenderArgs a = base_render_args(ctx);
+    a.cam.stride = 1, a.cam.GW = a.cam.W, a.cam.GH = a.cam.H;
+    a.model_slot = dslot.as<int32_t>(), a.poses = dpose.as<double>(), a.n = 1;
+    a.bbox = dbb.as<int4>(), a.cap = dcap.as<long long>();
+    a.dense_z = dz.as<double>(), a.dense_c = dc.as<double>(), a.dense_valid = dv.as<uint8_t>(), a.dense_owner = dow.as<int32_t>();
+    if ((e = launch_fill_dense(a.dense_z, a.dense_c, a.dense_valid, a.dense_owner, npix, ctx->stream)) ||
+        (e = launch_bbox(a, ctx->stream)) || (e = launch_render(a, ctx->render_smem, true, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 3;
+    if ((rc = d2h(ctx, zbuf, dz.p, npix * 8)) || (rc = d2h(ctx, cbuf, dc.p, npix * 24)) ||
+        (rc = d2h(ctx, valid, dv.p, npix)) || (rc = d2h(ctx, owner, dow.p, npix * 4)))
+      break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("rasterize: ") + cudaGetErrorString(e));
+  } while (0);
+  DevBuf* bufs[] = {&dz, &dc, &dv, &dow, &dslot, &dpose, &dbb, &dcap};
+  for (DevBuf* b : bufs) b->release();
+  return rc;
+}
+
+// ---- registration -----------------------------------------------------------
+
+int px_covariances(px_ctx* ctx, const double* points, int64_t n, int32_t k, double eps, double* cov_out) {
+  if (!ctx || !points || !cov_out) return fail(ctx, PX_E_ARG, "px_covariances: bad arguments");
+  if (k < 4 || k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k out of range [4,32]");
+  if (n <= k) return fail(ctx, PX_E_ARG, "need more than k points");
+  CU(cudaSetDevice(ctx->device));
+  DevBuf dp, dc, doff;
+  long long off[2] = {0, (long long)n};
+  int rc = 0;
+  do {
+    if ((rc = h2d(ctx, dp, points, (size_t)n * 24))) break;
+    if ((rc = h2d(ctx, doff, off, sizeof off))) break;
+    cudaError_t e = dc.ensure((size_t)n * 72);
+    if (e) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    CovArgs a{1, doff.as<long long>(), nullptr, dp.as<double>(), dc.as<double>(), k, eps};
+    if ((e = launch_cov(a, n, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 1;
+    if ((rc = d2h(ctx, cov_out, dc.p, (size_t)n * 72))) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("covariances: ") + cudaGetErrorString(e));
+  } while (0);
+  dp.release(), dc.release(), doff.release();
+  return rc;
+}
+
+int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, const double* points, int32_t k,
+                      double eps) {
+  if (!ctx || n_targets < 0 || (n_targets && !offsets)) return fail(ctx, PX_E_ARG, "px_targets_upload: bad arguments");
+  if (k < 4 || k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k_covariance out of range [4,32]");
+  CU(cudaSetDevice(ctx->device));
+  const long long total = n_targets ? (long long)offsets[n_targets] : 0;
+  for (int i = 0; i < n_targets; ++i)
+    if (offsets[i + 1] < offsets[i] || offsets[i + 1] - offsets[i] > 0x7fffffff)
+      return fail(ctx, PX_E_ARG, "target offsets must be non-decreasing");
+  if (total && !points) return fail(ctx, PX_E_ARG, "target points is NULL");
+  std::vector<long long> off((size_t)n_targets + 1, 0);
+  for (int i = 0; i <= n_targets && n_targets; ++i) off[(size_t)i] = (long long)offsets[i];
+  if (int r = h2d(ctx, ctx->tgt_off, off.data(), off.size() * 8)) return r;
+  if (int r = h2d(ctx, ctx->tgt_pts, points, (size_t)total * 24)) return r;
+  CU(ctx->tgt_cov.ensure((size_t)std::max<long long>(total, 1) * 72));
+  ctx->n_targets = n_targets, ctx->tgt_total = total, ctx->tgt_k = k;
+  if (n_targets) {
+    CovArgs a{n_targets, ctx->tgt_off.as<long long>(), nullptr, ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>(), k, eps};
+    CU(launch_cov(a, total, ctx->stream));
+    ctx->launches += 1;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int px_targets_covariances(px_ctx* ctx, double* cov_out) {
+  if (!ctx || !cov_out) return fail(ctx, PX_E_ARG, "px_targets_covariances: bad arguments");
+  if (int r = d2h(ctx, cov_out, ctx->tgt_cov.p, (size_t)ctx->tgt_total * 72)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target_idx, const double* init_T,
+                    const px_gicp_cfg* cfg, double* out_T, int32_t* out_iters, int32_t* out_flags,
+                    double* out_residual, double* out_trace, int32_t* out_ntrace) {
+  if (!ctx || !sources || !cfg) return fail(ctx, PX_E_ARG, "px_refine_batch: bad arguments");
+  const int64_t n = sources->s.n;
+  if (n && !target_idx) return fail(ctx, PX_E_ARG, "target_idx is NULL");
+  if (int r = check_gicp(ctx, *cfg)) return r;
+  for (int64_t i = 0; i < n; ++i)
+    if (target_idx[i] < 0 || target_idx[i] >= ctx->n_targets) return fail(ctx, PX_E_ARG, "target index out of range");
+  if (n == 0) return 0;
+  CU(cudaSetDevice(ctx->device));
+  if (int r = ensure_refine_scratch(ctx, sources->s.total_cap)) return r;
+  DevBuf dti, dinit, dT, dit, dfl, dres, dtr, dnt;
+  int rc = 0;
+  do {
+    cudaError_t e;
+    if ((rc = h2d(ctx, dti, target_idx, (size_t)n * 4))) break;
+    if (init_T && (rc = h2d(ctx, dinit, init_T, (size_t)n * 96))) break;
+    if ((e = dT.ensure((size_t)n * 96)) || (e = dit.ensure((size_t)n * 4)) || (e = dfl.ensure((size_t)n * 4)) ||
+        (e = dnt.ensure((size_t)n * 4)) || (out_residual && (e = dres.ensure((size_t)n * 8))) ||
+        (out_trace && (e = dtr.ensure((size_t)n * 16 * (size_t)std::max(cfg->max_iterations, 1))))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    RefineArgs a{};
+    a.src = clouds_dev(sources->s);
+    a.tgt = TargetsDev{ctx->n_targets, ctx->tgt_off.as<long long>(), ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>()};
+    a.target_idx = dti.as<int32_t>();
+    a.init_T = init_T ? dinit.as<double>() : nullptr;
+    a.cfg = gicp_dev(*cfg);
+    a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
+    a.out_resid = out_residual ? dres.as<double>() : nullptr;
+    a.out_trace = out_trace ? dtr.as<double>() : nullptr;
+    a.out_ntrace = dnt.as<int32_t>();
+    if ((e = launch_refine(a, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 1;
+    if ((rc = d2h(ctx, out_T, dT.p, (size_t)n * 96)) || (rc = d2h(ctx, out_iters, dit.p, (size_t)n * 4)) ||
+        (rc = d2h(ctx, out_flags, dfl.p, (size_t)n * 4)) || (rc = d2h(ctx, out_ntrace, dnt.p, (size_t)n * 4)) ||
+        (out_residual && (rc = d2h(ctx, out_residual, dres.p, (size_t)n * 8))) ||
+        (out_trace && (rc = d2h(ctx, out_trace, dtr.p, (size_t)n * 16 * (size_t)cfg->max_iterations))))
+      break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("refine: ") + cudaGetErrorString(e));
+  } while (0);
+  DevBuf* bufs[] = {&dti, &dinit, &dT, &dit, &dfl, &dres, &dtr, &dnt};
+  for (DevBuf* b : bufs) b->release();
+  return rc;
+}
+
+// ---- cost ---------------------------------------------------------------------
+
+int px_cost_batch(px_ctx* ctx, const px_clouds* rendered, const int32_t* object_ids, const double* cyl_poses,
+                  double delta, double tau_c, int32_t use_color, int32_t* j_o, int32_t* j_r) {
+  if (!ctx || !rendered || !j_o || !j_r) return fail(ctx, PX_E_ARG, "px_cost_batch: bad arguments");
+  if (!ctx->have_scene) return fail(ctx, PX_E_ARG, "no scene uploaded");
+  const int64_t n = rendered->s.n;
+  if (n == 0) return 0;
+  if (!object_ids) return fail(ctx, PX_E_ARG, "object_ids is NULL");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<int32_t> slots;
+  if (int r = slots_from_ids(ctx, object_ids, n, slots)) return r;
+  if (int r = sync_models(ctx)) return r;
+  DevBuf dslot, dpose, djo, djr;
+  int rc = 0;
+  do {
+    cudaError_t e;
+    if ((rc = h2d(ctx, dslot, slots.data(), (size_t)n * 4))) break;
+    if (cyl_poses && (rc = h2d(ctx, dpose, cyl_poses, (size_t)n * 96))) break;
+    if ((e = djo.ensure((size_t)n * 4)) || (e = djr.ensure((size_t)n * 4))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    if ((rc = run_cost(ctx, rendered->s, dslot.as<int32_t>(), cyl_poses ? dpose.as<double>() : nullptr, delta, tau_c,
+                       use_color, djo.as<int32_t>(), djr.as<int32_t>(), nullptr, nullptr)))
+      break;
+    if ((rc = d2h(ctx, j_o, djo.p, (size_t)n * 4)) || (rc = d2h(ctx, j_r, djr.p, (size_t)n * 4))) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("cost: ") + cudaGetErrorString(e));
+  } while (0);
+  dslot.release(), dpose.release(), djo.release(), djr.release();
+  return rc;
+}
+
+int px_rendered_cost(px_ctx* ctx, const double* rp, const double* rlab, int64_t n_r, const double* op,
+                     const double* olab, int64_t n_obs, double delta, double tau_c, int32_t use_color, int32_t* j_r,
+                     uint8_t* explained) {
+  if (!ctx || !j_r || n_r < 0 || n_obs < 0 || (n_obs && !explained)) return fail(ctx, PX_E_ARG, "px_rendered_cost: bad arguments");
+  if (n_obs) memset(explained, 0, (size_t)n_obs);
+  if (n_r == 0) {
+    *j_r = 0;
+    return 0;
+  }
+  if (n_obs == 0) {
+    *j_r = (int32_t)n_r;
+    return 0;
+  }
+  CU(cudaSetDevice(ctx->device));
+  DevBuf drp, drl, dop, dol, dex, djr;
+  int rc = 0;
+  do {
+    cudaError_t e;
+    if ((rc = h2d(ctx, drp, rp, (size_t)n_r * 24)) || (rc = h2d(ctx, drl, rlab, (size_t)n_r * 24)) ||
+        (rc = h2d(ctx, dop, op, (size_t)n_obs * 24)) || (rc = h2d(ctx, dol, olab, (size_t)n_obs * 24)))
+      break;
+    if ((e = dex.ensure((size_t)n_obs)) || (e = djr.ensure(4)) || (e = cudaMemsetAsync(dex.p, 0, (size_t)n_obs, ctx->stream)) ||
+        (e = cudaMemsetAsync(djr.p, 0, 4, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    GenericCostArgs a{drp.as<double>(), drl.as<double>(), (int)n_r, dop.as<double>(), dol.as<double>(), (long long)n_obs,
+                      delta * delta, tau_c, use_color, dex.as<uint8_t>(), djr.as<int32_t>()};
+    if ((e = launch_generic_cost(a, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 1;
+    if ((rc = d2h(ctx, j_r, djr.p, 4)) || (rc = d2h(ctx, explained, dex.p, (size_t)n_obs))) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("rendered_cost: ") + cudaGetErrorString(e));
+  } while (0);
+  DevBuf* bufs[] = {&drp, &drl, &dop, &dol, &dex, &djr};
+  for (DevBuf* b : bufs) b->release();
+  return rc;
+}
+
+int px_knn(px_ctx* ctx, const double* q, int64_t nq, const double* t, int64_t nt, int32_t k, int64_t* idx, double* d2) {
+  if (!ctx || nq < 0 || nt < 0 || k < 1 || (nq && (!q || !idx || !d2))) return fail(ctx, PX_E_ARG, "px_knn: bad arguments");
+  if (k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k > 32");
+  if (nq == 0) return 0;
+  CU(cudaSetDevice(ctx->device));
+  DevBuf dq, dt, di, dd;
+  int rc = 0;
+  do {
+    cudaError_t e;
+    if ((rc = h2d(ctx, dq, q, (size_t)nq * 24)) || (rc = h2d(ctx, dt, t, (size_t)nt * 24))) break;
+    if ((e = di.ensure((size_t)nq * k * 8)) || (e = dd.ensure((size_t)nq * k * 8))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    KnnArgs a{dq.as<double>(), (long long)nq, dt.as<double>(), (long long)nt, k, di.as<long long>(), dd.as<double>()};
+    if ((e = launch_knn(a, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 1;
+    if ((rc = d2h(ctx, idx, di.p, (size_t)nq * k * 8)) || (rc = d2h(ctx, d2, dd.p, (size_t)nq * k * 8))) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, std::string("knn: ") + cudaGetErrorString(e));
+  } while (0);
+  dq.release(), dt.release(), di.release(), dd.release();
+  return rc;
+}
+
+// ---- fused search -------------------------------------------------------------
+
+int px_search_upload(px_ctx* ctx, int64_t n, const int32_t* object_ids, const double* poses, const int32_t* target_idx,
+                     const int32_t* rank) {
+  if (!ctx || n < 0 || (n && (!object_ids || !poses || !rank))) return fail(ctx, PX_E_ARG, "px_search_upload: bad arguments");
+  if (n > 0x7fffffff) return fail(ctx, PX_E_LIMIT, "more than 2^31 candidates in one call");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<int32_t> slots;
+  if (int r = slots_from_ids(ctx, object_ids, n, slots)) return r;
+  if (int r = h2d(ctx, ctx->c_slot, slots.data(), (size_t)n * 4)) return r;
+  if (int r = h2d(ctx, ctx->c_pose, poses, (size_t)n * 96)) return r;
+  if (int r = h2d(ctx, ctx->c_rank, rank, (size_t)n * 4)) return r;
+  ctx->have_tidx = target_idx != nullptr;
+  if (target_idx)
+    if (int r = h2d(ctx, ctx->c_tidx, target_idx, (size_t)n * 4)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));  // `slots` is stack-owned
+  ctx->n_cand = n;
+  return 0;
+}
+
+static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64_t hi, bool timed) {
+  const int64_t n = hi - lo;
+  if (n <= 0) return 0;
+  const int32_t* slot = ctx->c_slot.as<int32_t>() + lo;
+  const double* pose_in = ctx->c_pose.as<double>() + 12 * lo;
+  double* pose_ref = ctx->r_pose.as<double>() + 12 * lo;
+  long long total = 0;
+  if (timed) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+  if (int r = size_clouds(ctx, ctx->clouds, slot, pose_in, n, &total)) return r;
+  const long long per_slot = 56 + (cfg->refine ? 148 : 0);
+  if (total * per_slot > ctx->scratch_budget && n > 1024) {
+    const int64_t mid = lo + n / 2;
+    if (int r = search_range(ctx, cfg, lo, mid, false)) return r;
+    return search_range(ctx, cfg, mid, hi, false);
+  }
+  if (int r = render_clouds(ctx, ctx->clouds, slot, pose_in, n, cfg->occluder_marking, cfg->delta)) return r;
+  CU(cudaMemcpyAsync(ctx->r_nfirst.as<int32_t>() + lo, ctx->clouds.count.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (timed) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+  const double* cost_pose = pose_in;
+  if (cfg->refine) {
+    if (int r = ensure_refine_scratch(ctx, total)) return r;
+    RefineArgs a{};
+    a.src = clouds_dev(ctx->clouds);
+    a.tgt = TargetsDev{ctx->n_targets, ctx->tgt_off.as<long long>(), ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>()};
+    a.target_idx = ctx->c_tidx.as<int32_t>() + lo;
+    a.cfg = gicp_dev(cfg->gicp);
+    a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.out_T = ctx->r_T.as<double>() + 12 * lo;
+    a.out_iters = ctx->r_iters.as<int32_t>() + lo, a.out_flags = ctx->r_flags.as<int32_t>() + lo;
+    a.poses_in = pose_in, a.poses_out = pose_ref;
+    a.mode3dof = cfg->mode3dof;
+    memcpy(a.c2w, cfg->cam_to_world, sizeof a.c2w);
+    memcpy(a.w2c, cfg->world_to_cam, sizeof a.w2c);
+    a.c2w_vec_order = cfg->c2w_vec_order, a.w2c_vec_order = cfg->w2c_vec_order, a.fixed_z = cfg->fixed_z;
+    CU(launch_refine(a, ctx->stream));
+    ctx->launches += 1;
+    if (timed) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+    if (int r = size_clouds(ctx, ctx->clouds, slot, pose_ref, n, &total)) return r;
+    if (int r = render_clouds(ctx, ctx->clouds, slot, pose_ref, n, cfg->occluder_marking, cfg->delta)) return r;
+    cost_pose = pose_ref;
+  } else {
+    CU(cudaMemcpyAsync(pose_ref, pose_in, (size_t)n * 96, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (timed) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+  }
+  CU(cudaMemcpyAsync(ctx->r_nfinal.as<int32_t>() + lo, ctx->clouds.count.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (timed) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+  if (int r = run_cost(ctx, ctx->clouds, slot, cfg->mode3dof ? cost_pose : nullptr, cfg->delta, cfg->tau_c, cfg->use_color,
+                       ctx->r_jo.as<int32_t>() + lo, ctx->r_jr.as<int32_t>() + lo, ctx->c_rank.as<int32_t>() + lo,
+                       ctx->r_key.as<unsigned long long>()))
+    return r;
+  if (timed) CU(cudaEventRecord(ctx->ev[4], ctx->stream));
+  return 0;
+}
+
+int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
+  if (!ctx || !cfg) return fail(ctx, PX_E_ARG, "px_search_run: bad arguments");
+  if (!ctx->have_scene) return fail(ctx, PX_E_ARG, "no scene uploaded");
+  if (!ctx->organised) return fail(ctx, PX_E_ARG, "scene cloud is not the organised stride-grid cloud");
+  CU(cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n_cand;
+  if (cfg->refine) {
+    if (!ctx->have_tidx) return fail(ctx, PX_E_ARG, "refine requested but no target_idx uploaded");
+    if (int r = check_gicp(ctx, cfg->gicp)) return r;
+  }
+  if (int r = sync_models(ctx)) return r;
+  const size_t nn = (size_t)std::max<int64_t>(n, 1);
+  CU(ctx->r_T.ensure(nn * 96));
+  CU(ctx->r_pose.ensure(nn * 96));
+  DevBuf* ib[] = {&ctx->r_iters, &ctx->r_flags, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst, &ctx->r_nfinal};
+  for (DevBuf* b : ib) CU(b->ensure(nn * 4));
+  CU(ctx->r_key.ensure(sizeof(unsigned long long) * std::max<size_t>(ctx->models.size(), 1)));
+  CU(cudaMemsetAsync(ctx->r_key.p, 0xff, sizeof(unsigned long long) * std::max<size_t>(ctx->models.size(), 1), ctx->stream));
+  CU(cudaMemsetAsync(ctx->r_iters.p, 0, nn * 4, ctx->stream));
+  CU(cudaMemsetAsync(ctx->r_flags.p, 0, nn * 4, ctx->stream));
+  if (!cfg->refine) {
+    // identity corrections
+    std::vector<double> I((size_t)n * 12, 0.0);
+    for (int64_t i = 0; i < n; ++i) I[12 * i] = I[12 * i + 5] = I[12 * i + 10] = 1.0;
+    if (n) CU(cudaMemcpyAsync(ctx->r_T.p, I.data(), (size_t)n * 96, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  for (double& m : ctx->stage_ms) m = 0.0;
+  if (n == 0) return 0;
+  if (int r = search_range(ctx, cfg, 0, n, true)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  float ms;
+  // events are only recorded on the un-split path; a split run reports zeros
+  if (cudaEventQuery(ctx->ev[4]) == cudaSuccess) {
+    for (int i = 0; i < 4; ++i)
+      if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) ctx->stage_ms[i] = ms;
+  }
+  cudaGetLastError();
+  return 0;
+}
+
+int px_search_download(px_ctx* ctx, double* refined, double* reg_T, int32_t* iters, int32_t* flags, int32_t* j_o,
+                       int32_t* j_r, int32_t* n_first, int32_t* n_final, uint64_t* best_key, double stage_ms[4]) {
+  if (!ctx) return PX_E_ARG;
+  const size_t n = (size_t)ctx->n_cand;
+  if (int r = d2h(ctx, refined, ctx->r_pose.p, n * 96)) return r;
+  if (int r = d2h(ctx, reg_T, ctx->r_T.p, n * 96)) return r;
+  if (int r = d2h(ctx, iters, ctx->r_iters.p, n * 4)) return r;
+  if (int r = d2h(ctx, flags, ctx->r_flags.p, n * 4)) return r;
+  if (int r = d2h(ctx, j_o, ctx->r_jo.p, n * 4)) return r;
+  if (int r = d2h(ctx, j_r, ctx->r_jr.p, n * 4)) return r;
+  if (int r = d2h(ctx, n_first, ctx->r_nfirst.p, n * 4)) return r;
+  if (int r = d2h(ctx, n_final, ctx->r_nfinal.p, n * 4)) return r;
+  if (int r = d2h(ctx, best_key, ctx->r_key.p, ctx->models.size() * 8)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (stage_ms)
+    for (int i = 0; i < 4; ++i) stage_ms[i] = ctx->stage_ms[i];
+  return 0;
+}
+
+}  // extern "C"

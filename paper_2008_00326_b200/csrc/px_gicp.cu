@@ -1,0 +1,529 @@
+// px_gicp.cu -- k-NN covariances and batched many-to-many GICP refinement.
+//
+// Replaces registration._covariance_kernel / _gicp_linearize / _gicp_objective /
+// gicp_align / _m2m_task (reference pkg/src/rvpose/registration.py:109-511) and
+// the refine-apply + 3-DoF re-lift of search.py:291-301 for a whole batch.
+//
+// One warp per candidate.  Everything that is order-sensitive in the reference
+// is evaluated in the reference's order:
+//   * nearest neighbour = lexicographic min of (d2, index) (strict `<` scan);
+//   * the 36 H / 6 g / f0 accumulators are sums over the source index in
+//     ascending order: per-point terms are computed lane-parallel, staged
+//     through shared memory (transposed, padded), and 43 lanes then add their
+//     entry serially in index order -- bit-identical to the scalar loop;
+//   * the fixed-association objective is summed in index order via shuffles.
+// numpy products in gicp_align (r_step @ r_cur, r_step @ t_cur) use the host
+// BLAS fused orders (px_common.cuh); np.linalg.solve is LAPACK dgesv's
+// algorithm (partial-pivot LU); orthonormalize is the polar projection.
+// Compiled with -fmad=false.
+#include "px_kernels.h"
+
+namespace px {
+
+enum { F_OK = 0, F_TOO_FEW = 1, F_DEGENERATE = 2, F_SINGULAR = 3, F_NO_DECREASE = 4 };
+
+// registration.py:117-216 for point i of a cloud of n points (n > k)
+__device__ void cov_point(const double* __restrict__ pts, int n, int i, int k, double eps, double* __restrict__ out) {
+  double nd[PX_KCOV_MAX];
+  int ni[PX_KCOV_MAX];
+  const double xi = pts[3 * i], yi = pts[3 * i + 1], zi = pts[3 * i + 2];
+  int cnt = 0;
+  double worst = CUDART_INF;
+  for (int j = 0; j < n; ++j) {
+    const double dx = pts[3 * j] - xi, dy = pts[3 * j + 1] - yi, dz = pts[3 * j + 2] - zi;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    int pos;
+    if (cnt < k)
+      pos = cnt++;
+    else if (d2 < worst)
+      pos = k - 1;
+    else
+      continue;
+    while (pos > 0 && nd[pos - 1] > d2) nd[pos] = nd[pos - 1], ni[pos] = ni[pos - 1], --pos;
+    nd[pos] = d2, ni[pos] = j;
+    if (cnt == k) worst = nd[k - 1];
+  }
+  double mx = 0.0, my = 0.0, mz = 0.0;
+  for (int q = 0; q < k; ++q) mx += pts[3 * ni[q]], my += pts[3 * ni[q] + 1], mz += pts[3 * ni[q] + 2];
+  const double kd = (double)k;
+  mx /= kd, my /= kd, mz /= kd;
+  double a00 = 0, a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0;
+  for (int q = 0; q < k; ++q) {
+    const double dx = pts[3 * ni[q]] - mx, dy = pts[3 * ni[q] + 1] - my, dz = pts[3 * ni[q] + 2] - mz;
+    a00 += dx * dx, a01 += dx * dy, a02 += dx * dz, a11 += dy * dy, a12 += dy * dz, a22 += dz * dz;
+  }
+  double a[3][3], vm[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  a[0][0] = a00 / kd, a[0][1] = a01 / kd, a[0][2] = a02 / kd;
+  a[1][1] = a11 / kd, a[1][2] = a12 / kd, a[2][2] = a22 / kd;
+  a[1][0] = a[0][1], a[2][0] = a[0][2], a[2][1] = a[1][2];
+  for (int sweep = 0; sweep < 16; ++sweep) {
+    const double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+    const double scale = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]) + 1e-300;
+    if (off <= 1e-14 * scale) break;
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int q = p + 1; q < 3; ++q) {
+        const double apq = a[p][q];
+        if (apq == 0.0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+        double tt;
+        if (theta >= 0.0)
+          tt = 1.0 / (theta + sqrt(theta * theta + 1.0));
+        else
+          tt = -1.0 / (-theta + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double tmp = a[r][p];
+          a[r][p] = c * tmp - s * a[r][q];
+          a[r][q] = s * tmp + c * a[r][q];
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double tmp = a[p][r];
+          a[p][r] = c * tmp - s * a[q][r];
+          a[q][r] = s * tmp + c * a[q][r];
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double tmp = vm[r][p];
+          vm[r][p] = c * tmp - s * vm[r][q];
+          vm[r][q] = s * tmp + c * vm[r][q];
+        }
+      }
+  }
+  double dmin = a[0][0], x = vm[0][0], y = vm[1][0], z = vm[2][0];
+  if (a[1][1] < dmin) dmin = a[1][1], x = vm[0][1], y = vm[1][1], z = vm[2][1];
+  if (a[2][2] < dmin) dmin = a[2][2], x = vm[0][2], y = vm[1][2], z = vm[2][2];
+  const double f = 1.0 - eps;
+  out[0] = 1.0 - f * x * x, out[1] = -f * x * y, out[2] = -f * x * z;
+  out[3] = out[1], out[4] = 1.0 - f * y * y, out[5] = -f * y * z;
+  out[6] = out[2], out[7] = out[5], out[8] = 1.0 - f * z * z;
+}
+
+// one CTA per cloud, threads over its points
+__global__ void __launch_bounds__(128) cov_kernel(CovArgs a) {
+  const int c = blockIdx.x;
+  const long long off = a.offset[c];
+  const int n = a.count ? a.count[c] : (int)(a.offset[c + 1] - off);
+  if (n <= a.k) return;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cov_point(a.points + 3 * off, n, i, a.k, a.eps, a.cov + 9 * (off + i));
+}
+
+cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
+  if (a.n_clouds == 0) return cudaSuccess;
+  cov_kernel<<<a.n_clouds, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+
+#define STAGE_LD 33
+#define WARP_SM_DOUBLES (43 * STAGE_LD + 43 + 8)
+
+// LAPACK dgesv restated: partial-pivot LU, first maximal |a| wins, zero pivot = singular
+__device__ int solve6(const double* h, double diag_add, const double* g, double* x) {
+  double a[6][7];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int j = 0; j < 6; ++j) a[i][j] = h[6 * i + j] + (i == j ? diag_add : 0.0);
+    a[i][6] = g[i];
+  }
+  for (int c = 0; c < 6; ++c) {
+    int p = c;
+    double best = fabs(a[c][c]);
+    for (int i = c + 1; i < 6; ++i)
+      if (fabs(a[i][c]) > best) best = fabs(a[i][c]), p = i;
+    if (best == 0.0 || isnan(best)) return 1;
+    if (p != c)
+      for (int j = 0; j < 7; ++j) {
+        const double tmp = a[c][j];
+        a[c][j] = a[p][j], a[p][j] = tmp;
+      }
+    const double inv = 1.0 / a[c][c];
+    for (int i = c + 1; i < 6; ++i) {
+      const double l = a[i][c] * inv;
+      a[i][c] = l;
+      for (int j = c + 1; j < 7; ++j) a[i][j] = a[i][j] - l * a[c][j];
+    }
+  }
+  for (int i = 5; i >= 0; --i) {
+    double s = a[i][6];
+    for (int j = i + 1; j < 6; ++j) s = s - a[i][j] * x[j];
+    x[i] = s / a[i][i];
+  }
+  return 0;
+}
+
+// registration.py:479-494
+__device__ int solve_normal_equations(const double* h, const double* g, double* xi) {
+  const double pi2 = CUDART_PI * CUDART_PI;
+  for (int damped = 0; damped < 2; ++damped) {
+    if (solve6(h, damped ? 1e-6 : 0.0, g, xi)) continue;
+    bool fin = true;
+    for (int i = 0; i < 6; ++i) fin = fin && isfinite(xi[i]);
+    if (fin && xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2] < pi2 &&
+        xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5] < 1.0)
+      return 0;
+  }
+  return 1;
+}
+
+// registration.py:341-361
+__device__ __forceinline__ void so3_exp_fast(double wx, double wy, double wz, double* o) {
+  const double theta2 = wx * wx + wy * wy + wz * wz, theta = sqrt(theta2);
+  double a, b;
+  if (theta < 1e-10)
+    a = 1.0, b = 0.5;
+  else
+    a = sin(theta) / theta, b = (1.0 - cos(theta)) / theta2;
+  o[0] = 1.0 + b * (-wz * wz - wy * wy);
+  o[1] = -a * wz + b * wx * wy;
+  o[2] = a * wy + b * wx * wz;
+  o[3] = a * wz + b * wx * wy;
+  o[4] = 1.0 + b * (-wz * wz - wx * wx);
+  o[5] = -a * wx + b * wy * wz;
+  o[6] = -a * wy + b * wx * wz;
+  o[7] = a * wx + b * wy * wz;
+  o[8] = 1.0 + b * (-wy * wy - wx * wx);
+}
+
+// registration.py:364-384
+__device__ __forceinline__ void renorm_rotation(const double* r, double* o) {
+  const double n0 = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  const double x0 = r[0] / n0, x1 = r[1] / n0, x2 = r[2] / n0;
+  double y0 = r[3], y1 = r[4], y2 = r[5];
+  const double dot = x0 * y0 + x1 * y1 + x2 * y2;
+  y0 -= dot * x0, y1 -= dot * x1, y2 -= dot * x2;
+  const double ny = sqrt(y0 * y0 + y1 * y1 + y2 * y2);
+  y0 = y0 / ny, y1 = y1 / ny, y2 = y2 / ny;
+  o[0] = x0, o[1] = x1, o[2] = x2, o[3] = y0, o[4] = y1, o[5] = y2;
+  o[6] = x1 * y2 - x2 * y1, o[7] = x2 * y0 - x0 * y2, o[8] = x0 * y1 - x1 * y0;
+}
+
+// nearest rotation (geometry.py:82-89): polar factor by Newton iteration
+__device__ __forceinline__ void orthonormalize3(const double* r, double* x) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) x[i] = r[i];
+  for (int it = 0; it < 3; ++it) {
+    const double c[9] = {x[4] * x[8] - x[5] * x[7], x[5] * x[6] - x[3] * x[8], x[3] * x[7] - x[4] * x[6],
+                         x[2] * x[7] - x[1] * x[8], x[0] * x[8] - x[2] * x[6], x[1] * x[6] - x[0] * x[7],
+                         x[1] * x[5] - x[2] * x[4], x[2] * x[3] - x[0] * x[5], x[0] * x[4] - x[1] * x[3]};
+    const double det = x[0] * c[0] + x[1] * c[1] + x[2] * c[2];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) x[i] = 0.5 * (x[i] + c[i] / det);
+  }
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// fixed-association objective, registration.py:387-407; uniform result in all lanes
+__device__ double gicp_objective(const double* __restrict__ src, int n, const double* __restrict__ tgt,
+                                 const int32_t* __restrict__ corr, const double* __restrict__ wb,
+                                 const double* r, const double* t, int lane) {
+  double f = 0.0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    double term = 0.0;
+    bool on = false;
+    if (i < n) {
+      const int j = corr[i];
+      if (j >= 0) {
+        on = true;
+        const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
+        const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+        const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+        const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+        const double dx = tgt[3 * j] - px, dy = tgt[3 * j + 1] - py, dz = tgt[3 * j + 2] - pz;
+        const double* w = wb + 9 * (size_t)i;
+        const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
+        const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
+        const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
+        term = dx * wd0 + dy * wd1 + dz * wd2;
+      }
+    }
+    unsigned vm = __ballot_sync(0xffffffffu, on);
+    while (vm) {
+      const int j = __ffs(vm) - 1;
+      vm &= vm - 1;
+      f += shfl_d(term, j);
+    }
+  }
+  return f;
+}
+
+__global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs a) {
+  extern __shared__ double sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * PX_GICP_WARPS + wid;
+  if (c >= a.src.n) return;
+  double* stage = sm + (size_t)wid * WARP_SM_DOUBLES;  // [43][STAGE_LD]
+  double* hg = stage + 43 * STAGE_LD;                  // [43]: H (36), g (6), f0
+  double* xis = hg + 43;                               // [6] + status
+
+  const int n = a.src.count[c];
+  const long long off = a.src.offset[c];
+  const double* src = a.src.points + 3 * off;
+  double* ca = a.src_cov + 9 * off;
+  double* wb = a.w_buf + 9 * off;
+  int32_t* corr = a.corr + off;
+  const int ti = a.target_idx[c];
+  const long long toff = a.tgt.offset[ti];
+  const int nt = (int)(a.tgt.offset[ti + 1] - toff);
+  const double* tgt = a.tgt.points + 3 * toff;
+  const double* cb = a.tgt.cov + 9 * toff;
+  const GicpCfgDev cfg = a.cfg;
+
+  double r[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t[3] = {0, 0, 0};
+  if (a.init_T) {
+    const double* T0 = a.init_T + 12 * (size_t)c;
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) r[3 * i + j] = T0[4 * i + j];
+      t[i] = T0[4 * i + 3];
+    }
+  }
+  int failure = F_OK, iters = 0, conv = 0;
+  double* trace = a.out_trace ? a.out_trace + 2 * (size_t)cfg.max_iter * c : nullptr;
+  int n_trace = 0;
+
+  if (n <= cfg.k_cov || nt <= cfg.k_cov) {
+    failure = F_TOO_FEW;  // registration.py:504-510
+  } else {
+    for (int i = lane; i < n; i += 32) cov_point(src, n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
+    __syncwarp();
+    double r_try[9], t_try[3];
+    for (int it = 1; it <= cfg.max_iter; ++it) {
+      iters = it;
+      // ---- linearise (registration.py:233-338) ----
+      double acc0 = 0.0, acc1 = 0.0;
+      int n_corr = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        bool on = false;
+        if (i < n) {
+          const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
+          const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+          const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+          const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+          double best = CUDART_INF;
+          int bj = -1;
+#pragma unroll 4
+          for (int j = 0; j < nt; ++j) {
+            const double dx = tgt[3 * j] - px, dy = tgt[3 * j + 1] - py, dz = tgt[3 * j + 2] - pz;
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < best) best = d2, bj = j;
+          }
+          int cj = -1;
+          if (bj >= 0 && !(best > cfg.gate2)) {
+            const double* cai = ca + 9 * (size_t)i;
+            const double* cbj = cb + 9 * (size_t)bj;
+            double rc[9], m[9];
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+#pragma unroll
+              for (int v = 0; v < 3; ++v) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < 3; ++w) s += r[3 * u + w] * cai[3 * w + v];
+                rc[3 * u + v] = s;
+              }
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+#pragma unroll
+              for (int v = 0; v < 3; ++v) {
+                double s = 0.0;
+#pragma unroll
+                for (int w = 0; w < 3; ++w) s += rc[3 * u + w] * r[3 * v + w];
+                m[3 * u + v] = cbj[3 * u + v] + s;
+              }
+            const double det = (m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                                m[2] * (m[3] * m[7] - m[4] * m[6]));
+            if (!(det <= 0.0) && isfinite(det)) {
+              cj = bj;
+              on = true;
+              const double inv_det = 1.0 / det;
+              double w[9];
+              w[0] = (m[4] * m[8] - m[5] * m[7]) * inv_det;
+              w[1] = (m[2] * m[7] - m[1] * m[8]) * inv_det;
+              w[2] = (m[1] * m[5] - m[2] * m[4]) * inv_det;
+              w[3] = (m[5] * m[6] - m[3] * m[8]) * inv_det;
+              w[4] = (m[0] * m[8] - m[2] * m[6]) * inv_det;
+              w[5] = (m[2] * m[3] - m[0] * m[5]) * inv_det;
+              w[6] = (m[3] * m[7] - m[4] * m[6]) * inv_det;
+              w[7] = (m[1] * m[6] - m[0] * m[7]) * inv_det;
+              w[8] = (m[0] * m[4] - m[1] * m[3]) * inv_det;
+              double* wo = wb + 9 * (size_t)i;
+#pragma unroll
+              for (int q = 0; q < 9; ++q) wo[q] = w[q];
+              const double dx = tgt[3 * bj] - px, dy = tgt[3 * bj + 1] - py, dz = tgt[3 * bj + 2] - pz;
+              const double J[3][6] = {{0.0, -pz, py, -1.0, 0.0, 0.0},
+                                      {pz, 0.0, -px, 0.0, -1.0, 0.0},
+                                      {-py, px, 0.0, 0.0, 0.0, -1.0}};
+              const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
+              const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
+              const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
+              stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
+#pragma unroll
+              for (int u = 0; u < 6; ++u)
+                stage[(36 + u) * STAGE_LD + lane] = -(J[0][u] * wd0 + J[1][u] * wd1 + J[2][u] * wd2);
+              double wj[3][6];
+#pragma unroll
+              for (int q = 0; q < 3; ++q)
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+                  wj[q][u] = w[3 * q] * J[0][u] + w[3 * q + 1] * J[1][u] + w[3 * q + 2] * J[2][u];
+#pragma unroll
+              for (int u = 0; u < 6; ++u)
+#pragma unroll
+                for (int v = 0; v < 6; ++v)
+                  stage[(6 * u + v) * STAGE_LD + lane] = J[0][u] * wj[0][v] + J[1][u] * wj[1][v] + J[2][u] * wj[2][v];
+            }
+          }
+          corr[i] = cj;
+        }
+        __syncwarp();  // stage writes visible to the summing lanes
+        unsigned vm = __ballot_sync(0xffffffffu, on);
+        n_corr += __popc(vm);
+        while (vm) {
+          const int j = __ffs(vm) - 1;
+          vm &= vm - 1;
+          acc0 += stage[lane * STAGE_LD + j];
+          if (lane < 11) acc1 += stage[(lane + 32) * STAGE_LD + j];
+        }
+        __syncwarp();
+      }
+      hg[lane] = acc0;
+      if (lane < 11) hg[32 + lane] = acc1;
+      __syncwarp();
+      const double f0 = hg[42];
+      if (n_corr < 6) {
+        failure = F_DEGENERATE;
+        break;
+      }
+      if (lane == 0) {
+        double xi0[6];
+        const int bad = solve_normal_equations(hg, hg + 36, xi0);
+        for (int q = 0; q < 6; ++q) xis[q] = xi0[q];
+        xis[6] = bad ? 1.0 : 0.0;
+      }
+      __syncwarp();
+      if (xis[6] != 0.0) {
+        failure = F_SINGULAR;
+        break;
+      }
+      double xi[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) xi[q] = xis[q];
+      __syncwarp();
+      // ---- step halving (registration.py:443-457) ----
+      bool accepted = false;
+      double scale = 1.0, f_try = 0.0;
+      for (int tr = 0; tr < 9; ++tr) {
+        double rs[9];
+        so3_exp_fast(scale * xi[0], scale * xi[1], scale * xi[2], rs);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            r_try[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
+          t_try[i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
+        }
+        f_try = gicp_objective(src, n, tgt, corr, wb, r_try, t_try, lane);
+        if (isfinite(f_try) && f_try <= f0) {
+          accepted = true;
+          break;
+        }
+        scale *= 0.5;
+      }
+      if (!accepted) {
+        failure = F_NO_DECREASE;
+        break;
+      }
+      renorm_rotation(r_try, r);
+      t[0] = t_try[0], t[1] = t_try[1], t[2] = t_try[2];
+      if (trace && lane == 0) trace[2 * (it - 1)] = f0, trace[2 * (it - 1) + 1] = f_try;
+      n_trace = it;
+      const double step_t2 = scale * scale * (xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+      const double step_r2 = scale * scale * (xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+      if (step_t2 < cfg.tol_t2 && step_r2 < cfg.tol_r2) {
+        conv = 1;
+        break;
+      }
+      if (it >= 5 && f0 > 0.0 && (f0 - f_try) <= 1e-4 * f0) break;
+    }
+  }
+  // ---- result transform (registration.py:473) ----
+  double T[12];
+  {
+    double ro[9];
+    orthonormalize3(r, ro);
+    if (failure == F_TOO_FEW) {
+#pragma unroll
+      for (int i = 0; i < 9; ++i) ro[i] = r[i];  // init returned untouched
+    }
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) T[4 * i + j] = ro[3 * i + j];
+      T[4 * i + 3] = t[i];
+    }
+  }
+  if (a.out_resid) {  // registration.py:59-67 (not used by the search path)
+    double sum = 0.0;
+    int cnt = 0;
+    if (failure != F_TOO_FEW) {
+      for (int i = lane; i < n; i += 32) {
+        double x, y, z;
+        apply_pose(T, src[3 * i], src[3 * i + 1], src[3 * i + 2], x, y, z);
+        double best = CUDART_INF;
+        for (int j = 0; j < nt; ++j) {
+          const double dx = tgt[3 * j] - x, dy = tgt[3 * j + 1] - y, dz = tgt[3 * j + 2] - z;
+          const double d2 = dx * dx + dy * dy + dz * dz;
+          if (d2 < best) best = d2;
+        }
+        if (best <= cfg.gate2) sum += best, ++cnt;
+      }
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o), cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0) a.out_resid[c] = cnt ? sqrt(sum / (double)cnt) : CUDART_INF;
+  }
+  if (lane == 0) {
+    for (int i = 0; i < 12; ++i) a.out_T[12 * (size_t)c + i] = T[i];
+    a.out_iters[c] = iters;
+    a.out_flags[c] = failure | (conv ? 0x100 : 0);
+    if (a.out_ntrace) a.out_ntrace[c] = n_trace;
+    if (a.poses_in) {  // search.py:291-301
+      const double* pin = a.poses_in + 12 * (size_t)c;
+      double cam[12];
+      if (failure == F_TOO_FEW && iters == 0) {
+        for (int i = 0; i < 12; ++i) cam[i] = pin[i];
+      } else {
+        compose_pose(T, pin, 0, cam);
+        if (a.mode3dof) {
+          double world[12];
+          compose_pose(a.c2w, cam, a.c2w_vec_order, world);
+          const double yaw = atan2(world[4], world[0]);  // registration.py:556
+          double y = fmod(yaw, 2.0 * CUDART_PI);         // geometry.py:98-105
+          if (y < 0.0) y += 2.0 * CUDART_PI;
+          if (y >= 2.0 * CUDART_PI) y -= 2.0 * CUDART_PI;
+          const double cy = cos(y), sy = sin(y);
+          const double lift[12] = {cy, -sy, 0.0, world[3], sy, cy, 0.0, world[7], 0.0, 0.0, 1.0, a.fixed_z};
+          compose_pose(a.w2c, lift, a.w2c_vec_order, cam);
+        }
+      }
+      for (int i = 0; i < 12; ++i) a.poses_out[12 * (size_t)c + i] = cam[i];
+    }
+  }
+}
+
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st) {
+  if (a.src.n == 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
+  cudaError_t e = cudaFuncSetAttribute(gicp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
+  gicp_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace px

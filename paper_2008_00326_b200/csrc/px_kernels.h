@@ -1,0 +1,172 @@
+// px_kernels.h -- kernel argument blocks and launchers shared by the libpx
+// translation units (internal; the public C-ABI is include/px.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "px_common.cuh"
+
+#define PX_RENDER_THREADS 128
+#define PX_TRI_SMEM 64      // meshes up to this many triangles use the per-pixel path
+#define PX_TILE_PIX 4096    // stride-grid pixels per shared-memory z tile (atomic path)
+#define PX_GICP_WARPS 8     // candidates (warps) per CTA in the GICP kernel
+#define PX_COST_WARPS 4
+#define PX_KCOV_MAX 32
+
+namespace px {
+
+struct ModelDev {
+  const double* verts;  // (V,3) object frame
+  const double* col;    // (V,3) linear-light colour
+  const int32_t* tris;  // (T,3)
+  int V, T;
+  int32_t object_id;
+  int pad_;
+  double cyl_r2, cyl_zmin, cyl_zmax;
+  double aabb_r;        // sqrt(cyl_r2) upper bound used only for screen bounds
+};
+
+struct RenderArgs {
+  Camera cam;
+  const ModelDev* models;
+  const int32_t* model_slot;  // (n)
+  const double* poses;        // (n,12)
+  int n;
+  int occluder_marking;
+  double delta_occ;
+  const double* obs_depth;    // (H,W)
+  const uint8_t* obs_valid;
+  const int32_t* obs_labels;
+  int4* bbox;                 // (n) out of K0 / in of K1
+  long long* cap;             // (n) out of K0
+  const long long* offset;    // (n) exclusive scan of cap
+  int32_t* count;             // (n) out
+  double* points;             // (sum cap,3)
+  double* lab;                // (sum cap,3)
+  int32_t* src_px;            // (sum cap,2)
+  // dense single-view output (px_rasterize)
+  double* dense_z;
+  double* dense_c;
+  uint8_t* dense_valid;
+  int32_t* dense_owner;
+};
+
+size_t render_smem_bytes(int V, int T);
+cudaError_t launch_bbox(const RenderArgs& a, cudaStream_t st);
+cudaError_t launch_render(const RenderArgs& a, size_t smem, bool dense, cudaStream_t st);
+cudaError_t launch_scan(const long long* in, long long* out_excl, long long* total, int n, cudaStream_t st);
+cudaError_t launch_fill_dense(double* z, double* c, uint8_t* valid, int32_t* owner, size_t npix, cudaStream_t st);
+
+struct GicpCfgDev {
+  int k_cov, max_iter;
+  double eps, tol_t2, tol_r2, gate2;
+};
+
+// ragged cloud batch on the device: candidate c owns slots [offset[c], offset[c]+count[c])
+struct CloudsDev {
+  int n;
+  const long long* offset;
+  const int32_t* count;
+  const double* points;
+  const double* lab;
+  const int32_t* src_px;
+};
+
+struct TargetsDev {
+  int n_targets;
+  const long long* offset;  // (n_targets+1)
+  const double* points;     // (sum,3)
+  const double* cov;        // (sum,9)
+};
+
+struct CovArgs {  // covariances of a list of clouds (targets), thread per point
+  int n_clouds;
+  const long long* offset;  // (n_clouds+1) or per-cloud offsets with counts
+  const int32_t* count;     // nullable: if null, count = offset[i+1]-offset[i]
+  const double* points;
+  double* cov;              // (sum,9)
+  int k;
+  double eps;
+};
+cudaError_t launch_cov(const CovArgs& a, long long total_points, cudaStream_t st);
+
+struct RefineArgs {
+  CloudsDev src;
+  TargetsDev tgt;
+  const int32_t* target_idx;  // (n)
+  const double* init_T;       // (n,12) or null = identity
+  GicpCfgDev cfg;
+  // scratch, indexed by the source slot offsets
+  double* src_cov;            // (sum cap,9)
+  double* w_buf;              // (sum cap,9)
+  int32_t* corr;              // (sum cap)
+  // outputs
+  double* out_T;              // (n,12) [orthonormalize(R)|t]
+  int32_t* out_iters;
+  int32_t* out_flags;         // low byte failure code, bit 8 converged
+  double* out_resid;          // nullable: rms residual (registration.py:59-67)
+  double* out_trace;          // nullable: (n, max_iter, 2) objective trace (f0, f_try)
+  int32_t* out_ntrace;        // nullable: accepted steps per candidate
+  // refine-apply (search.py:291-301); poses_in null => skip
+  const double* poses_in;     // (n,12) candidate poses
+  double* poses_out;          // (n,12) refined candidate poses
+  int mode3dof;
+  double c2w[12], w2c[12];
+  int c2w_vec_order, w2c_vec_order;
+  double fixed_z;
+};
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st);
+
+struct CostArgs {
+  CloudsDev ren;
+  Camera cam;
+  const ModelDev* models;
+  const int32_t* model_slot;   // (n)
+  const double* cyl_poses;     // (n,12) or null -> label mode
+  // organised observed cloud
+  const double* gx;            // (GH*GW) NaN where no point
+  const double* gy;
+  const double* gz;
+  const int32_t* gidx;         // (GH*GW) observed index or -1
+  const double* obs_lab;       // (n_obs,3)
+  const int32_t* obs_labels;   // (n_obs)
+  const int32_t* label_count;  // per model slot: count(obs_labels == oid)
+  double delta, delta2, tau_c;
+  int use_color;
+  uint32_t* bitmap;            // scratch: (#warp slots) x bitmap_words, zero on entry and exit
+  int bitmap_words;
+  int bitmap_slots;            // number of warp slots the bitmap scratch holds (multiple of PX_COST_WARPS)
+  int32_t* j_o;                // (n) out
+  int32_t* j_r;                // (n) out
+  // fused argmin (search.py:178-183): key = total<<32 | rank
+  const int32_t* rank;         // (n) rank of the candidate inside its object, nullable
+  unsigned long long* best_key;  // per model slot, nullable
+};
+cudaError_t launch_cost(const CostArgs& a, cudaStream_t st);
+
+struct KnnArgs {  // exact brute-force kNN, k <= PX_KCOV_MAX (neighbors.py:104-134)
+  const double* q;
+  long long nq;
+  const double* t;
+  long long nt;
+  int k;
+  long long* idx;  // (nq,k)
+  double* d2;      // (nq,k)
+};
+cudaError_t launch_knn(const KnnArgs& a, cudaStream_t st);
+
+struct GenericCostArgs {  // cost.py:91-135 on arbitrary (non-organised) clouds
+  const double* rp;
+  const double* rlab;
+  int n_r;
+  const double* op;
+  const double* olab;
+  long long n_obs;
+  double delta2, tau_c;
+  int use_color;
+  uint8_t* explained;  // (n_obs) zeroed by the caller
+  int32_t* j_r;        // single int, zeroed by the caller -> counts outliers
+};
+cudaError_t launch_generic_cost(const GenericCostArgs& a, cudaStream_t st);
+
+}  // namespace px

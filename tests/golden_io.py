@@ -1,0 +1,79 @@
+"""Load tests/golden/*.npz fixtures (written by oracle/make_golden.py from the
+reference itself) back into boundary types."""
+
+from __future__ import annotations
+
+import json
+import hashlib
+from functools import lru_cache
+from pathlib import Path
+
+import numpy as np
+
+from paper_2008_00326_b200 import (CameraIntrinsics, GicpConfig, InscribedCylinder, ObjectModel,
+                                   ObjectState, RigidTransform, SearchConfig, TriangleMesh)
+from paper_2008_00326_b200.model import frame_from_quantized
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+@lru_cache(maxsize=None)
+def load(name: str):
+    return dict(np.load(GOLDEN / f"{name}.npz", allow_pickle=False))
+
+
+def cloud_digest(points, source_pixel) -> np.ndarray:
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(points, dtype=np.float64).tobytes())
+    h.update(np.ascontiguousarray(source_pixel, dtype=np.int32).tobytes())
+    return np.frombuffer(h.digest(), dtype=np.uint8)
+
+
+def models_of(d) -> dict:
+    out = {}
+    for oid in d["model_ids"]:
+        oid = int(oid)
+        mesh = TriangleMesh(d[f"m{oid}_verts"], d[f"m{oid}_colors"], d[f"m{oid}_tris"])
+        r, z0, z1 = (float(x) for x in d[f"m{oid}_cyl"])
+        out[oid] = ObjectModel(oid, mesh, InscribedCylinder(r, z0, z1), bool(int(d[f"m{oid}_sym"])))
+    return out
+
+
+def frame_of(d):
+    fx, fy, cx, cy, w, h = d["intr"]
+    rot = d["cam_rot"] if int(d["cam_rot_c_contig"]) else np.asfortranarray(d["cam_rot"])
+    k = CameraIntrinsics(float(fx), float(fy), float(cx), float(cy), int(w), int(h),
+                         RigidTransform(rot, d["cam_t"]))
+    dets = [(int(i), tuple(float(x) for x in bb)) for i, bb in zip(d["det_ids"], d["det_bbox"])]
+    gt = [ObjectState(int(i), RigidTransform.from_matrix3x4(p)) for i, p in zip(d["gt_ids"], d["gt_pose"])]
+    return frame_from_quantized(d["col8"], d["depth_mm"], d["lab8"], k, dets, gt or None)
+
+
+def config_of(d, **overrides) -> SearchConfig:
+    c = json.loads(str(d["cfg_json"]))
+    c.pop("workers", None)
+    cfg = SearchConfig.from_dict(c)
+    if overrides:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, **overrides)
+    return cfg
+
+
+@lru_cache(maxsize=None)
+def scene(name: str):
+    """(fixture dict, frame, models, cfg, plan) for a search fixture."""
+    from paper_2008_00326_b200.search import plan_search
+
+    d = load(name)
+    frame, models, cfg = frame_of(d), models_of(d), config_of(d)
+    plan = plan_search(frame, models, cfg)
+    return d, frame, models, cfg, plan
+
+
+def pose_delta(a, b):
+    """(translation distance, rotation angle) between two stacks of 3x4 poses."""
+    a, b = np.asarray(a), np.asarray(b)
+    dt = np.linalg.norm(a[..., :, 3] - b[..., :, 3], axis=-1)
+    rel = np.einsum("...ij,...kj->...ik", a[..., :, :3], b[..., :, :3])
+    tr = np.clip((np.trace(rel, axis1=-2, axis2=-1) - 1.0) / 2.0, -1.0, 1.0)
+    return dt, np.arccos(tr)
