@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Headline benchmark: candidate poses scored / second through
+render -> GICP refine -> re-render -> cost -> argmin (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3] [--impl reference]
+
+A step = one pass of the hot path over one batch of candidates of the workload
+scene.  Workload (default `c3`): the cluttered five-box 3-DoF scene of
+BASELINE.json configs[2] (the committed, reference-generated, disk-round-tripped
+scene in tests/golden/c3_clutter_3dof.npz), workspace +-0.32 m, dt 0.025 m,
+dyaw 22.5 deg / N_gpus -> 58,320 candidates per GPU, ICP refinement on.
+Candidates are sharded across ranks by grid cell (weak scaling: per-GPU work is
+fixed); the only collective is an all_reduce(MIN) of the packed (cost, pose-id)
+keys, one uint64 per object.
+
+`value`  : inputs resident in HBM, timed with CUDA events on the launch stream.
+`e2e`    : same metric through the engine's C-ABI calls from HOST buffers:
+           scene + models + targets + candidate upload, search, result download.
+`--impl reference`: the CPU oracle port (the reference is pure Python and cannot
+           travel to the GPU box) on all host cores, on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "candidate poses scored/sec (render+ICP+cost)"
+UNIT = "poses/s"
+
+WORKLOADS = {
+    # name: (fixture, overrides per n_gpus -> SearchConfig kwargs)
+    "c1": ("c1_box_3dof", lambda n: dict(dyaw=np.radians(22.5) / n)),
+    "c2": ("c2_twocyl_color1", lambda n: dict(dt=0.04 / n)),
+    "c3": ("c3_clutter_3dof", lambda n: dict(dt=0.025, dyaw=np.radians(22.5) / n, max_proposals=None)),
+    "c3s": ("c3_clutter_3dof", lambda n: dict(dt=0.08, dyaw=np.radians(22.5) / n, max_proposals=None)),
+    "c4": ("c4_mixed_6dof", lambda n: dict(viewpoints=642 * n, n_inplane=36, z_step=0.01, max_proposals=None)),
+}
+
+
+def build_workload(name: str, n_gpus: int):
+    import golden_io as G
+    from paper_2008_00326_b200.search import plan_search
+
+    fixture, over = WORKLOADS[name]
+    d = G.load(fixture)
+    frame, models = G.frame_of(d), G.models_of(d)
+    cfg = dataclasses.replace(G.config_of(d), **over(n_gpus))
+    plan = plan_search(frame, models, cfg)
+    return frame, models, cfg, plan
+
+
+def shard_index(plan, rank: int, world: int) -> np.ndarray:
+    """Candidates of this rank: grid cells (3-DoF) / rotation blocks (6-DoF) dealt
+    round-robin so every target cloud stays on one rank and load is interleaved."""
+    if world == 1:
+        return np.arange(plan.n)
+    key = np.empty(plan.n, dtype=np.int64)
+    for oid in plan.active:
+        sel = np.nonzero(plan.flat_oid == oid)[0]
+        key[sel] = plan.proposal_sets[oid].provenance[plan.flat_local[sel], 0]
+    return np.nonzero(key % world == rank)[0]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.rows, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100", "-i", str(index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            pass
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[0])), mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refine):
+    """SURVEY.md 8(d) per-candidate algorithmic bytes, summed over the batch,
+    split per kernel.  f64 = 8 B, i32 = 4 B, bool = 1 B."""
+    V = np.array([models[int(o)].mesh.vertices.shape[0] for o in flat_oid], dtype=np.float64)
+    T = np.array([models[int(o)].mesh.triangles.shape[0] for o in flat_oid], dtype=np.float64)
+    n0, n1 = out.n_first.astype(np.float64), out.n_rendered.astype(np.float64)
+    it = out.iterations.astype(np.float64)
+    b_render0 = 96 + 48 * V + 12 * T + 13 * cap0 + 56 * n0
+    b_render1 = 96 + 48 * V + 12 * T + 13 * cap1 + 56 * n1
+    b_cov = 96 * n0
+    b_iter_sum = it * (104 * n0 + 344) + 96 * ncorr_sum.astype(np.float64)
+    b_cost = 56 * n1 + 48 * n1 + 25 * cap1 + 8   # n_m <= n_r, footprint ~ screen box of the final render
+    d = {"render": float(b_render0.sum()), "rerender": float(b_render1.sum()) if refine else 0.0,
+         "refine": float((b_cov + b_iter_sum).sum()) if refine else 0.0, "cost": float(b_cost.sum())}
+    d["total"] = sum(d.values())
+    return d
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+    hbm_peak, peak_src = (peaks["hbm_gbs"], "measured") if "hbm_gbs" in peaks else (6650.0, "fallback")
+
+    from paper_2008_00326_b200.engine import Engine
+
+    frame, models, cfg, plan = build_workload(args.workload, world)
+    idx = shard_index(plan, rank, world)
+    eng = Engine(local)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    sc = eng.search_cfg(plan)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    keys_t = torch.zeros(max(len(plan.active), 1), dtype=torch.int64, device="cuda")
+
+    def reduce_keys(out):
+        """The only collective: min over ranks of (total << 32 | rank-in-object) per object."""
+        if world > 1:
+            k = np.array([out.best_keys.get(oid, 2**63 - 1) & (2**63 - 1) for oid in plan.active], dtype=np.int64)
+            keys_t.copy_(torch.from_numpy(k))
+            dist.all_reduce(keys_t, op=dist.ReduceOp.MIN)
+
+    # ---- resident-input arm (`value`) ----
+    eng.prepare_plan(frame, models, plan)
+    n_local = eng.search_upload(plan, idx)
+    for _ in range(args.warmup):
+        eng.search_run(sc)
+    out = eng.search_download(n_local)
+    reduce_keys(out)
+    barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    launches0 = eng.launch_count()
+    step_ms, stage_ms = [], []
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed iterations (outside the event pair)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.search_run(sc)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        o = eng.search_download(n_local, full=False)
+        stage_ms.append(o.stage_millis)
+        reduce_keys(o)
+    barrier()
+    wall_s = time.perf_counter() - t_wall0
+    launches = eng.launch_count() - launches0
+    clocks = sampler.stop() if sampler else None
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        cnt = torch.tensor([n_local], dtype=torch.int64, device="cuda")
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        n_total = int(cnt.item())
+    else:
+        n_total = n_local
+    ms_per_step = total_ms / args.steps
+    value = n_total / (ms_per_step * 1e-3)
+
+    # ---- end-to-end arm (`e2e`): host buffers -> C-ABI -> host results, every step ----
+    barrier()
+    e2e_ms = []
+    h2d = d2h = 0
+    for s in range(max(2, min(args.steps, 5)) + 1):
+        t0 = time.perf_counter()
+        eng._scene_key = None
+        eng._model_keys.clear()
+        eng.prepare_plan(frame, models, plan)
+        eng.search_upload(plan, idx)
+        eng.search_run(sc)
+        o = eng.search_download(n_local)
+        reduce_keys(o)
+        torch.cuda.synchronize()
+        if s:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    k_ = frame.intrinsics
+    npix = k_.width * k_.height
+    h2d = (npix * 13 + len(plan.observed) * (24 + 24 + 8 + 4) + int(plan.target_offsets[-1]) * 24
+           + sum(m.mesh.vertices.size * 16 + m.mesh.triangles.size * 4 for m in models.values())
+           + n_local * (96 + 12))
+    d2h = n_local * (96 + 96 + 4 * 6) + 8 * len(plan.active)
+    e2e_t = float(np.median(e2e_ms)) * 1e-3
+    if world > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_value = n_total / e2e_t
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (GICP refine) ----
+    full = eng.search_download(n_local)
+    ncs, cap0, cap1 = eng.search_stats(n_local)
+    ab = algorithmic_bytes(n_local, models, plan.flat_oid[idx], full, ncs, cap0, cap1, cfg.refine)
+    st = {k: float(np.mean([s[k] for s in stage_ms])) for k in stage_ms[0]}
+    dom = max(st, key=st.get)
+    dom_ms = st[dom]
+    achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": {"refine": "gicp_kernel", "render": "render_kernel", "rerender": "render_kernel",
+                                          "cost": "cost_kernel"}[dom],
+                "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None,
+                "algorithmic_bytes_per_launch": ab[dom], "kernel_ms": dom_ms,
+                "whole_step_achieved": ab["total"] / (ms_per_step * 1e-3) / 1e9,
+                "whole_step_frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
+                "bytes_per_candidate": ab["total"] / max(n_local, 1)}
+
+    # ---- CPU baseline on a bounded sample of the same workload (rank 0, N=1 only) ----
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(frame, models, plan, idx, args.cpu_sample)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload][0]} scene, mode={cfg.mode}, refine={cfg.refine}, "
+                               f"candidates/GPU={n_local}, total={n_total}, stride={cfg.stride}, 640x480",
+                   "candidates_per_step": n_total, "sharding": "grid cells round-robin across ranks; all_reduce(MIN) of packed (cost,pose-id) keys",
+                   "l2": "256 MiB flush between timed steps; per-step scratch also exceeds L2"},
+        "stage_ms": st, "wall_s_timed_region": wall_s,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_t * 1e3},
+        "gpu_launches": int(launches),
+        "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
+        "mean_iterations": float(full.iterations.mean()), "mean_rendered_points": float(full.n_rendered.mean()),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sample_groups(plan, idx, sample: int) -> np.ndarray:
+    """Bounded CPU sample: whole target groups (all yaws of a grid cell / all
+    candidates sharing a GICP target) spaced uniformly over the step's candidates,
+    so the per-target covariance build is amortised exactly as in the full step."""
+    if len(idx) <= sample:
+        return idx
+    if plan.target_idx is None:
+        return idx[np.unique(np.round(np.linspace(0, len(idx) - 1, sample)).astype(int))]
+    t = plan.target_idx[idx]
+    groups = np.unique(t)
+    per = max(1.0, len(idx) / len(groups))
+    want = max(1, int(round(sample / per)))
+    chosen = groups[np.unique(np.round(np.linspace(0, len(groups) - 1, min(want, len(groups)))).astype(int))]
+    return idx[np.isin(t, chosen)]
+
+
+def cpu_baseline(frame, models, plan, idx, sample: int):
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    pick = sample_groups(plan, idx, sample)
+    O.run_plan(frame, models, plan, n_threads=cores, index=pick[:64])  # warm-up (page in, threads)
+    t0 = time.perf_counter()
+    out = O.run_plan(frame, models, plan, n_threads=cores, index=pick)
+    dt = time.perf_counter() - t0
+    return {"value": len(pick) / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{len(pick)} candidates (whole grid cells spaced uniformly) of the step's {len(idx)} (oracle/px_oracle.c, pthreads, "
+                      f"{dt:.1f} s)", "stage_ms": {k: float(v) for k, v in out.stage_millis.items()}}
+
+
+def run_reference(args):
+    """Reference arm: the reference's algorithm on the host cores.  The reference
+    package is pure Python/numba and is not present on the GPU box, so this arm
+    runs its C restatement (oracle/px_oracle.c), pinned to the reference's own
+    outputs by tests/test_oracle_golden.py."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    frame, models, cfg, plan = build_workload(args.workload, world)
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    idx = np.arange(plan.n)
+    pick = sample_groups(plan, idx, args.cpu_sample)
+    for _ in range(args.warmup):
+        O.run_plan(frame, models, plan, n_threads=cores, index=pick[:128])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out = O.run_plan(frame, models, plan, n_threads=cores, index=pick)
+        times.append(time.perf_counter() - t0)
+    ms = float(np.mean(times)) * 1e3
+    value = len(pick) / (ms * 1e-3)
+    sample = f"{len(pick)} candidates (whole grid cells spaced uniformly) of the workload's {plan.n} per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload][0]} scene, mode={cfg.mode}, refine={cfg.refine}",
+                   "candidates_per_step": len(pick)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=3000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    import __graft_entry__ as ge
+
+    if int(os.environ.get("LOCAL_RANK", "0")) == 0:
+        ge.build()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -166,6 +166,11 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg);
 int px_search_download(px_ctx* ctx, double* refined_poses, double* reg_T, int32_t* iters, int32_t* flags,
                        int32_t* j_o, int32_t* j_r, int32_t* n_first, int32_t* n_final,
                        uint64_t* best_key_per_model, double stage_ms[4]);
+/* Work counters of the last px_search_run for roofline accounting (any pointer
+ * may be NULL): per candidate, the sum over GICP iterations of the
+ * correspondence count, and the stride-grid pixels inside the screen bounding
+ * box of the first / final render (n_c, A_g). */
+int px_search_stats(px_ctx* ctx, int32_t* ncorr_sum, int64_t* cap_first, int64_t* cap_final);
 /* Number of models uploaded and their ids in slot order (for best_key_per_model). */
 int px_model_count(const px_ctx* ctx);
 int px_model_ids(const px_ctx* ctx, int32_t* ids);

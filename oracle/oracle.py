@@ -255,10 +255,21 @@ def run_plan(frame, models, plan, n_threads=None, index=None):
     sc.n_threads = int(n_threads or os.cpu_count() or 1)
     sc.cloud_cap = scene.cap
     if cfg.refine and plan.target_offsets is not None:
-        toff = np.ascontiguousarray(plan.target_offsets, dtype=np.int64)
-        tpts = _f(plan.target_points)
-        tix = np.ascontiguousarray(tidx, dtype=np.int32)
-        ntg = toff.shape[0] - 1
+        # only targets referenced by these candidates get covariances (m2m_gicp
+        # builds them per distinct target of the call, registration.py:533-540)
+        used = np.unique(tidx)
+        remap = np.full(plan.target_offsets.shape[0] - 1, -1, dtype=np.int32)
+        remap[used] = np.arange(used.size, dtype=np.int32)
+        sizes = np.diff(plan.target_offsets)[used]
+        toff = np.zeros(used.size + 1, dtype=np.int64)
+        np.cumsum(sizes, out=toff[1:])
+        if used.size == remap.size:
+            tpts = _f(plan.target_points)
+        else:
+            tpts = _f(np.concatenate([plan.target_points[plan.target_offsets[t]:plan.target_offsets[t + 1]]
+                                      for t in used])) if used.size else np.zeros((0, 3))
+        tix = np.ascontiguousarray(remap[tidx], dtype=np.int32)
+        ntg = used.size
     else:
         toff, tpts, tix, ntg = np.zeros(1, dtype=np.int64), np.zeros((0, 3)), np.zeros(max(n, 1), dtype=np.int32), 0
     refined, regT = np.empty((n, 3, 4)), np.empty((n, 3, 4))

@@ -88,7 +88,7 @@ struct px_ctx {
   // search scratch / results
   CloudStore clouds;
   DevBuf src_cov, w_buf, corr, total_dev;
-  DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap;
+  DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1;
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
   double stage_ms[4] = {0, 0, 0, 0};
@@ -319,7 +319,7 @@ void px_ctx_destroy(px_ctx* ctx) {
                     &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
-                    &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap};
+                    &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
   for (DevBuf* b : bufs) b->release();
   ctx->clouds.release();
   for (auto& ev : ctx->ev)
@@ -864,6 +864,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     return search_range(ctx, cfg, mid, hi, false);
   }
   if (int r = render_clouds(ctx, ctx->clouds, slot, pose_in, n, cfg->occluder_marking, cfg->delta)) return r;
+  CU(cudaMemcpyAsync(ctx->r_cap0.as<long long>() + lo, ctx->clouds.cap.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   CU(cudaMemcpyAsync(ctx->r_nfirst.as<int32_t>() + lo, ctx->clouds.count.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (timed) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
   const double* cost_pose = pose_in;
@@ -877,6 +878,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
     a.out_T = ctx->r_T.as<double>() + 12 * lo;
     a.out_iters = ctx->r_iters.as<int32_t>() + lo, a.out_flags = ctx->r_flags.as<int32_t>() + lo;
+    a.out_ncorr_sum = ctx->r_ncorr.as<int32_t>() + lo;
     a.poses_in = pose_in, a.poses_out = pose_ref;
     a.mode3dof = cfg->mode3dof;
     memcpy(a.c2w, cfg->cam_to_world, sizeof a.c2w);
@@ -893,6 +895,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     if (timed) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
   }
   CU(cudaMemcpyAsync(ctx->r_nfinal.as<int32_t>() + lo, ctx->clouds.count.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->r_cap1.as<long long>() + lo, ctx->clouds.cap.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   if (timed) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
   if (int r = run_cost(ctx, ctx->clouds, slot, cfg->mode3dof ? cost_pose : nullptr, cfg->delta, cfg->tau_c, cfg->use_color,
                        ctx->r_jo.as<int32_t>() + lo, ctx->r_jr.as<int32_t>() + lo, ctx->c_rank.as<int32_t>() + lo,
@@ -916,8 +919,11 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
   CU(ctx->r_T.ensure(nn * 96));
   CU(ctx->r_pose.ensure(nn * 96));
-  DevBuf* ib[] = {&ctx->r_iters, &ctx->r_flags, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst, &ctx->r_nfinal};
+  DevBuf* ib[] = {&ctx->r_iters, &ctx->r_flags, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst, &ctx->r_nfinal, &ctx->r_ncorr};
   for (DevBuf* b : ib) CU(b->ensure(nn * 4));
+  CU(ctx->r_cap0.ensure(nn * 8));
+  CU(ctx->r_cap1.ensure(nn * 8));
+  CU(cudaMemsetAsync(ctx->r_ncorr.p, 0, nn * 4, ctx->stream));
   CU(ctx->r_key.ensure(sizeof(unsigned long long) * std::max<size_t>(ctx->models.size(), 1)));
   CU(cudaMemsetAsync(ctx->r_key.p, 0xff, sizeof(unsigned long long) * std::max<size_t>(ctx->models.size(), 1), ctx->stream));
   CU(cudaMemsetAsync(ctx->r_iters.p, 0, nn * 4, ctx->stream));
@@ -959,6 +965,16 @@ int px_search_download(px_ctx* ctx, double* refined, double* reg_T, int32_t* ite
   CU(cudaStreamSynchronize(ctx->stream));
   if (stage_ms)
     for (int i = 0; i < 4; ++i) stage_ms[i] = ctx->stage_ms[i];
+  return 0;
+}
+
+int px_search_stats(px_ctx* ctx, int32_t* ncorr_sum, int64_t* cap_first, int64_t* cap_final) {
+  if (!ctx) return PX_E_ARG;
+  const size_t n = (size_t)ctx->n_cand;
+  if (int r = d2h(ctx, ncorr_sum, ctx->r_ncorr.p, n * 4)) return r;
+  if (int r = d2h(ctx, cap_first, ctx->r_cap0.p, n * 8)) return r;
+  if (int r = d2h(ctx, cap_final, ctx->r_cap1.p, n * 8)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 

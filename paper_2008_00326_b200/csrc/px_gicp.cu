@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs 
   int failure = F_OK, iters = 0, conv = 0;
   double* trace = a.out_trace ? a.out_trace + 2 * (size_t)cfg.max_iter * c : nullptr;
   int n_trace = 0;
+  int ncorr_sum = 0;
 
   if (n <= cfg.k_cov || nt <= cfg.k_cov) {
     failure = F_TOO_FEW;  // registration.py:504-510
@@ -398,6 +399,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs 
       if (lane < 11) hg[32 + lane] = acc1;
       __syncwarp();
       const double f0 = hg[42];
+      ncorr_sum += n_corr;
       if (n_corr < 6) {
         failure = F_DEGENERATE;
         break;
@@ -492,6 +494,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs 
     a.out_iters[c] = iters;
     a.out_flags[c] = failure | (conv ? 0x100 : 0);
     if (a.out_ntrace) a.out_ntrace[c] = n_trace;
+    if (a.out_ncorr_sum) a.out_ncorr_sum[c] = ncorr_sum;
     if (a.poses_in) {  // search.py:291-301
       const double* pin = a.poses_in + 12 * (size_t)c;
       double cam[12];

@@ -107,6 +107,7 @@ struct RefineArgs {
   double* out_resid;          // nullable: rms residual (registration.py:59-67)
   double* out_trace;          // nullable: (n, max_iter, 2) objective trace (f0, f_try)
   int32_t* out_ntrace;        // nullable: accepted steps per candidate
+  int32_t* out_ncorr_sum;     // nullable: sum over iterations of the correspondence count (roofline accounting)
   // refine-apply (search.py:291-301); poses_in null => skip
   const double* poses_in;     // (n,12) candidate poses
   double* poses_out;          // (n,12) refined candidate poses

@@ -340,6 +340,13 @@ class Engine:
         out.best_keys = {int(i): int(k) for i, k in zip(ids[:nm], keys[:nm])}
         return out
 
+    def search_stats(self, n):
+        nc = np.zeros(n, dtype=np.int32)
+        c0, c1 = np.zeros(n, dtype=np.int64), np.zeros(n, dtype=np.int64)
+        rc = self.lib.px_search_stats(self.ctx, N.ptr(nc, N.i32p), N.ptr(c0, N.i64p), N.ptr(c1, N.i64p))
+        N.check(self.ctx, rc, "px_search_stats")
+        return nc, c0, c1
+
     def prepare_plan(self, frame, models, plan):
         self.upload_scene(frame, plan.cfg.stride, plan.observed, plan.obs_labels)
         self.upload_models({oid: models[oid] for oid in plan.active})
