@@ -119,9 +119,16 @@ int px_rasterize(px_ctx* ctx, int32_t object_id, const double pose3x4[12], doubl
 /* estimate_covariances for one cloud; n must exceed k (else PX_E_ARG). */
 int px_covariances(px_ctx* ctx, const double* points, int64_t n, int32_t k, double epsilon, double* cov_out);
 /* Target clouds of m2m_gicp: offsets (n_targets+1), points (offsets[n],3).
- * Covariances are built once per distinct target on the device. */
+ * Covariances (cfg->k_covariance, cfg->epsilon) and the nearest-neighbour grid
+ * (cfg->max_correspondence_distance) are built once per distinct target on the
+ * device; px_refine_batch / px_search_run must be called with the same cfg.
+ * obs_index (offsets[n]) optionally gives, for every target point, its index in
+ * the uploaded scene's observed cloud (ascending inside each target, as
+ * search._build_targets produces, search.py:393-426): the targets are then
+ * searched as organised pixel grids instead of by linear scans.  Results are
+ * identical either way. */
 int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, const double* points,
-                      int32_t k_covariance, double epsilon);
+                      const int64_t* obs_index /* nullable */, const px_gicp_cfg* cfg);
 int px_targets_covariances(px_ctx* ctx, double* cov_out); /* (offsets[n],9), for tests */
 /* m2m_gicp: one source cloud per entry, target_idx into the uploaded targets,
  * init_T (n,12) or NULL = identity.  Outputs (any may be NULL): out_T (n,12)

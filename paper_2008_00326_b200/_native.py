@@ -56,7 +56,7 @@ _SIGS = {
     "px_clouds_free": (None, [vp, vp]),
     "px_rasterize": (C.c_int, [vp, C.c_int32, f64p, f64p, f64p, u8p, i32p]),
     "px_covariances": (C.c_int, [vp, f64p, C.c_int64, C.c_int32, C.c_double, f64p]),
-    "px_targets_upload": (C.c_int, [vp, C.c_int32, i64p, f64p, C.c_int32, C.c_double]),
+    "px_targets_upload": (C.c_int, [vp, C.c_int32, i64p, f64p, i64p, C.POINTER(GicpCfg)]),
     "px_targets_covariances": (C.c_int, [vp, f64p]),
     "px_refine_batch": (C.c_int, [vp, vp, i32p, f64p, C.POINTER(GicpCfg), f64p, i32p, i32p, f64p,
                                   f64p, i32p]),

@@ -48,8 +48,9 @@ struct ModelHost {
 struct CloudStore {  // ragged per-candidate clouds with capacity slots
   int64_t n = 0;
   long long total_cap = 0;
-  DevBuf bbox, cap, offset, count, points, lab, src;
-  void release() { bbox.release(), cap.release(), offset.release(), count.release(), points.release(), lab.release(), src.release(); }
+  bool organised = false;  // slot_map / bbox valid (rendered on the device)
+  DevBuf bbox, cap, offset, count, points, lab, src, slot_map;
+  void release() { bbox.release(), cap.release(), offset.release(), count.release(), points.release(), lab.release(), src.release(), slot_map.release(); }
 };
 
 }  // namespace
@@ -69,7 +70,7 @@ struct px_ctx {
   Camera cam{};
   int64_t n_obs = 0;
   DevBuf depth, valid, labels, obs_pts, obs_lab, obs_labels, gx, gy, gz, gidx;
-  std::vector<int32_t> h_obs_labels;
+  std::vector<int32_t> h_obs_labels, h_obs_src;
   // models
   std::vector<ModelHost*> models;
   std::map<int32_t, int> slot_of;
@@ -80,7 +81,9 @@ struct px_ctx {
   int n_targets = 0;
   long long tgt_total = 0;
   int tgt_k = 0;
-  DevBuf tgt_off, tgt_pts, tgt_cov;
+  double tgt_gate = 0.0;
+  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_near, tgt_bits, tgt_org, tgt_map, tgt_pix;
+  bool tgt_organised = false;
   // resident candidates
   int64_t n_cand = 0;
   bool have_tidx = false;
@@ -190,12 +193,15 @@ int render_clouds(px_ctx* ctx, CloudStore& cs, const int32_t* slot_dev, const do
   CU(cs.points.ensure(sizeof(double) * 3 * tot));
   CU(cs.lab.ensure(sizeof(double) * 3 * tot));
   CU(cs.src.ensure(sizeof(int32_t) * 2 * tot));
+  CU(cs.slot_map.ensure(sizeof(int32_t) * tot));
+  cs.organised = true;
   RenderArgs a = base_render_args(ctx);
   a.model_slot = slot_dev, a.poses = pose_dev, a.n = (int)n;
   a.occluder_marking = occl, a.delta_occ = delta_occ;
   a.bbox = cs.bbox.as<int4>(), a.cap = cs.cap.as<long long>(), a.offset = cs.offset.as<long long>();
   a.count = cs.count.as<int32_t>();
   a.points = cs.points.as<double>(), a.lab = cs.lab.as<double>(), a.src_px = cs.src.as<int32_t>();
+  a.slot_map = cs.slot_map.as<int32_t>();
   CU(launch_render(a, ctx->render_smem, false, ctx->stream));
   ctx->launches += 1;
   return 0;
@@ -209,6 +215,8 @@ CloudsDev clouds_dev(const CloudStore& cs) {
   d.points = cs.points.as<double>();
   d.lab = cs.lab.as<double>();
   d.src_px = cs.src.as<int32_t>();
+  d.slot_map = cs.organised ? cs.slot_map.as<int32_t>() : nullptr;
+  d.bbox = cs.organised ? cs.bbox.as<int4>() : nullptr;
   return d;
 }
 
@@ -263,7 +271,8 @@ int check_gicp(px_ctx* ctx, const px_gicp_cfg& g) {
   if (g.k_covariance < 4 || g.k_covariance > PX_KCOV_MAX)
     return fail(ctx, PX_E_LIMIT, "k_covariance must lie in [4, " + std::to_string(PX_KCOV_MAX) + "]");
   if (g.max_iterations < 0) return fail(ctx, PX_E_ARG, "max_iterations < 0");
-  if (ctx->tgt_k != g.k_covariance) return fail(ctx, PX_E_ARG, "targets were uploaded with a different k_covariance");
+  if (ctx->tgt_k != g.k_covariance || ctx->tgt_gate != g.max_correspondence_distance)
+    return fail(ctx, PX_E_ARG, "targets were uploaded with a different k_covariance / max_correspondence_distance");
   return 0;
 }
 
@@ -316,7 +325,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
-                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
+                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_near, &ctx->tgt_bits, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
@@ -363,6 +372,11 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   c.fx = intr[0], c.fy = intr[1], c.cx = intr[2], c.cy = intr[3];
   c.W = W, c.H = H, c.stride = stride;
   c.GW = (W + stride - 1) / stride, c.GH = (H + stride - 1) / stride;
+  {
+    // bound of 1 + a^2 + b^2 over all pixel centres of the image (normalised coordinates)
+    const double am = std::max(c.cx, (double)W - c.cx) / c.fx, bm = std::max(c.cy, (double)H - c.cy) / c.fy;
+    c.ray_k = (double)stride / (std::max(c.fx, c.fy) * std::sqrt(1.0 + am * am + bm * bm)) * (1.0 - 1e-9);
+  }
   const size_t npix = (size_t)H * W;
   if (int r = h2d(ctx, ctx->depth, depth, npix * sizeof(double))) return r;
   if (int r = h2d(ctx, ctx->valid, valid, npix)) return r;
@@ -372,6 +386,8 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   if (int r = h2d(ctx, ctx->obs_labels, obs_labels, (size_t)n_obs * 4)) return r;
   ctx->n_obs = n_obs;
   ctx->h_obs_labels.assign(obs_labels, obs_labels + n_obs);
+  if (obs_src_px) ctx->h_obs_src.assign(obs_src_px, obs_src_px + 2 * n_obs);
+  else ctx->h_obs_src.clear();
   // organised-grid view: valid iff every source pixel sits on the stride grid in
   // strictly increasing row-major order (what raster.frame_to_cloud produces)
   const size_t ng = (size_t)c.GW * c.GH;
@@ -625,7 +641,8 @@ int px_covariances(px_ctx* ctx, const double* points, int64_t n, int32_t k, doub
       rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
       break;
     }
-    CovArgs a{1, doff.as<long long>(), nullptr, dp.as<double>(), dc.as<double>(), k, eps};
+    CovArgs a{};
+    a.n_clouds = 1, a.offset = doff.as<long long>(), a.points = dp.as<double>(), a.cov = dc.as<double>(), a.k = k, a.eps = eps;
     if ((e = launch_cov(a, n, ctx->stream))) {
       rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
       break;
@@ -639,10 +656,26 @@ int px_covariances(px_ctx* ctx, const double* points, int64_t n, int32_t k, doub
   return rc;
 }
 
-int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, const double* points, int32_t k,
-                      double eps) {
-  if (!ctx || n_targets < 0 || (n_targets && !offsets)) return fail(ctx, PX_E_ARG, "px_targets_upload: bad arguments");
+static TargetsDev targets_dev(px_ctx* ctx) {
+  TargetsDev t{};
+  t.n_targets = ctx->n_targets;
+  t.offset = ctx->tgt_off.as<long long>();
+  t.points = ctx->tgt_pts.as<double>();
+  t.cov = ctx->tgt_cov.as<double>();
+  t.near = ctx->tgt_near.as<TgtNear>();
+  t.near_bits = ctx->tgt_bits.as<uint32_t>();
+  t.org = ctx->tgt_organised ? ctx->tgt_org.as<TgtOrg>() : nullptr;
+  t.tmap = ctx->tgt_map.as<int32_t>();
+  return t;
+}
+
+int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, const double* points,
+                      const int64_t* obs_index, const px_gicp_cfg* cfg) {
+  if (!ctx || !cfg || n_targets < 0 || (n_targets && !offsets)) return fail(ctx, PX_E_ARG, "px_targets_upload: bad arguments");
+  const int k = cfg->k_covariance;
+  const double gate = cfg->max_correspondence_distance;
   if (k < 4 || k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k_covariance out of range [4,32]");
+  if (!(gate > 0.0)) return fail(ctx, PX_E_ARG, "max_correspondence_distance must be positive");
   CU(cudaSetDevice(ctx->device));
   const long long total = n_targets ? (long long)offsets[n_targets] : 0;
   for (int i = 0; i < n_targets; ++i)
@@ -651,16 +684,108 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   if (total && !points) return fail(ctx, PX_E_ARG, "target points is NULL");
   std::vector<long long> off((size_t)n_targets + 1, 0);
   for (int i = 0; i <= n_targets && n_targets; ++i) off[(size_t)i] = (long long)offsets[i];
+
+  // (1) near-bit grids: AABB grown by pad >= gate, cell h = gate/8 coarsened to the cell budget
+  std::vector<TgtNear> nears((size_t)n_targets);
+  long long word_total = 0;
+  const double pad = gate * (1.0 + 1e-6) + 1e-9;
+  for (int t = 0; t < n_targets; ++t) {
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    const long long a = off[(size_t)t], b = off[(size_t)t + 1];
+    for (long long i = a; i < b; ++i)
+      for (int d = 0; d < 3; ++d) {
+        const double v = points[3 * i + d];
+        if (!std::isfinite(v)) return fail(ctx, PX_E_ARG, "non-finite target point");
+        if (i == a || v < lo[d]) lo[d] = v;
+        if (i == a || v > hi[d]) hi[d] = v;
+      }
+    double h = gate / 8.0;
+    int nx, ny, nz;
+    for (;;) {
+      nx = (int)std::floor((hi[0] - lo[0] + 2 * pad) / h) + 2;
+      ny = (int)std::floor((hi[1] - lo[1] + 2 * pad) / h) + 2;
+      nz = (int)std::floor((hi[2] - lo[2] + 2 * pad) / h) + 2;
+      if ((long long)nx * ny * nz <= PX_GRID_MAX_CELLS) break;
+      h *= 1.1;
+    }
+    TgtNear& g = nears[(size_t)t];
+    g.ox = lo[0] - pad, g.oy = lo[1] - pad, g.oz = lo[2] - pad, g.inv_h = 1.0 / h;
+    g.nx = nx, g.ny = ny, g.nz = nz;
+    g.rd = (int)std::floor(gate / h) + 1;
+    g.bit_off = word_total;
+    word_total += ((long long)nx * ny * nz + 31) / 32;
+  }
+
+  // (2) organised views: valid when every target is an index-ascending subset of the
+  // uploaded scene's organised observed cloud
+  bool org = obs_index != nullptr && ctx->have_scene && ctx->organised && !ctx->h_obs_src.empty();
+  std::vector<TgtOrg> orgs((size_t)n_targets);
+  std::vector<int32_t> tmap, tpix;
+  if (org) {
+    const int st = ctx->cam.stride;
+    tpix.resize((size_t)total);
+    long long map_total = 0;
+    for (int t = 0; t < n_targets && org; ++t) {
+      const long long a = off[(size_t)t], b = off[(size_t)t + 1];
+      int x0 = 1 << 30, y0 = 1 << 30, x1 = -1, y1 = -1;
+      long long prev = -1;
+      for (long long i = a; i < b; ++i) {
+        const long long oi = obs_index[i];
+        if (oi <= prev || oi >= ctx->n_obs) {
+          org = false;
+          break;
+        }
+        prev = oi;
+        const int gx = ctx->h_obs_src[2 * oi] / st, gy = ctx->h_obs_src[2 * oi + 1] / st;
+        x0 = std::min(x0, gx), x1 = std::max(x1, gx), y0 = std::min(y0, gy), y1 = std::max(y1, gy);
+      }
+      TgtOrg& o = orgs[(size_t)t];
+      if (b > a) o.gx0 = x0, o.gy0 = y0, o.w = x1 - x0 + 1, o.h = y1 - y0 + 1;
+      else o.gx0 = o.gy0 = 0, o.w = 1, o.h = 1;
+      o.map_off = map_total;
+      map_total += (long long)o.w * o.h;
+    }
+    if (org) {
+      tmap.assign((size_t)map_total, -1);
+      for (int t = 0; t < n_targets; ++t) {
+        const TgtOrg& o = orgs[(size_t)t];
+        const long long a = off[(size_t)t], b = off[(size_t)t + 1];
+        for (long long i = a; i < b; ++i) {
+          const long long oi = obs_index[i];
+          const int cell = (ctx->h_obs_src[2 * oi + 1] / st - o.gy0) * o.w + (ctx->h_obs_src[2 * oi] / st - o.gx0);
+          tmap[(size_t)(o.map_off + cell)] = (int32_t)(i - a);
+          tpix[(size_t)i] = cell;
+        }
+      }
+    }
+  }
+  ctx->tgt_organised = org;
+
   if (int r = h2d(ctx, ctx->tgt_off, off.data(), off.size() * 8)) return r;
   if (int r = h2d(ctx, ctx->tgt_pts, points, (size_t)total * 24)) return r;
-  CU(ctx->tgt_cov.ensure((size_t)std::max<long long>(total, 1) * 72));
-  ctx->n_targets = n_targets, ctx->tgt_total = total, ctx->tgt_k = k;
-  if (n_targets) {
-    CovArgs a{n_targets, ctx->tgt_off.as<long long>(), nullptr, ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>(), k, eps};
-    CU(launch_cov(a, total, ctx->stream));
-    ctx->launches += 1;
+  if (int r = h2d(ctx, ctx->tgt_near, nears.data(), nears.size() * sizeof(TgtNear))) return r;
+  if (org) {
+    if (int r = h2d(ctx, ctx->tgt_org, orgs.data(), orgs.size() * sizeof(TgtOrg))) return r;
+    if (int r = h2d(ctx, ctx->tgt_map, tmap.data(), tmap.size() * 4)) return r;
+    if (int r = h2d(ctx, ctx->tgt_pix, tpix.data(), tpix.size() * 4)) return r;
   }
-  CU(cudaStreamSynchronize(ctx->stream));
+  const size_t tot1 = (size_t)std::max<long long>(total, 1);
+  CU(ctx->tgt_cov.ensure(tot1 * 72));
+  CU(ctx->tgt_bits.ensure((size_t)std::max<long long>(word_total, 1) * 4));
+  ctx->n_targets = n_targets, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = gate;
+  if (n_targets) {
+    CovArgs a{};
+    a.n_clouds = n_targets, a.offset = ctx->tgt_off.as<long long>(), a.count = nullptr;
+    a.points = ctx->tgt_pts.as<double>(), a.cov = ctx->tgt_cov.as<double>(), a.k = k, a.eps = cfg->epsilon;
+    if (org) a.org = ctx->tgt_org.as<TgtOrg>(), a.tmap = ctx->tgt_map.as<int32_t>(), a.tpix = ctx->tgt_pix.as<int32_t>();
+    a.ray_k = ctx->cam.ray_k;
+    CU(launch_cov(a, total, ctx->stream));
+    NearBuildArgs nb{n_targets, ctx->tgt_off.as<long long>(), ctx->tgt_pts.as<double>(), ctx->tgt_near.as<TgtNear>(),
+                     ctx->tgt_bits.as<uint32_t>()};
+    CU(launch_target_near(nb, ctx->stream));
+    ctx->launches += 2;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));  // host staging vectors are stack-owned
   return 0;
 }
 
@@ -697,10 +822,11 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
     }
     RefineArgs a{};
     a.src = clouds_dev(sources->s);
-    a.tgt = TargetsDev{ctx->n_targets, ctx->tgt_off.as<long long>(), ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>()};
+    a.tgt = targets_dev(ctx);
     a.target_idx = dti.as<int32_t>();
     a.init_T = init_T ? dinit.as<double>() : nullptr;
     a.cfg = gicp_dev(*cfg);
+    a.cam = ctx->cam;
     a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
     a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
     a.out_resid = out_residual ? dres.as<double>() : nullptr;
@@ -872,9 +998,10 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     if (int r = ensure_refine_scratch(ctx, total)) return r;
     RefineArgs a{};
     a.src = clouds_dev(ctx->clouds);
-    a.tgt = TargetsDev{ctx->n_targets, ctx->tgt_off.as<long long>(), ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>()};
+    a.tgt = targets_dev(ctx);
     a.target_idx = ctx->c_tidx.as<int32_t>() + lo;
     a.cfg = gicp_dev(cfg->gicp);
+    a.cam = ctx->cam;
     a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
     a.out_T = ctx->r_T.as<double>() + 12 * lo;
     a.out_iters = ctx->r_iters.as<int32_t>() + lo, a.out_flags = ctx->r_flags.as<int32_t>() + lo;

@@ -57,6 +57,7 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 struct Camera {
   double fx, fy, cx, cy;
   int W, H, stride, GW, GH;  // GW/GH: stride-grid dimensions ceil(W/stride), ceil(H/stride)
+  double ray_k;              // stride / (max(fx,fy) * sqrt(max over the image of 1+a^2+b^2)) * (1 - 1e-9)
 };
 
 }  // namespace px

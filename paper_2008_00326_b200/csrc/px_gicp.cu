@@ -102,13 +102,151 @@ __device__ void cov_point(const double* __restrict__ pts, int n, int i, int k, d
   out[6] = out[2], out[7] = out[5], out[8] = 1.0 - f * z * z;
 }
 
-// one CTA per cloud, threads over its points
+// ---------------------------------------------------------------------------
+// Organised views.  Rendered clouds and GICP targets are subsets of a pixel grid
+// (stride-grid pixels of the candidate's screen box / of the observed frame), so
+// neighbourhoods can be enumerated by pixel rings.  Everything below is EXACT:
+// a ring search stops only when the distance already found is strictly smaller
+// than a lower bound on the distance to every pixel not yet visited.
+//
+// Bound: p = z (a, b, 1) in normalised image coordinates; a point on the ray of a
+// pixel whose normalised offset from p is (da, db) is at least
+// z * sqrt(da^2 + db^2) / sqrt(1 + a_j^2 + b_j^2) away.  Camera::ray_k folds the
+// stride, max(fx, fy), the image-wide bound on 1 + a^2 + b^2 and a 1e-9 safety
+// factor: a pixel >= m grid steps away (Chebyshev) is >= z * m * ray_k distant.
+
+struct OrgView {
+  const double* pts;   // (n,3) points in local-index order (row-major pixel order)
+  const int32_t* map;  // (h,w) local index or -1
+  int w, h;
+};
+
+// k nearest (d2, index)-lexicographic neighbours of point i sitting at map cell
+// (cx, cy); identical to the reference's brute-force insertion scan
+// (registration.py:117-142).  nd/ni come back sorted ascending.
+__device__ __forceinline__ void knn_ring(const OrgView& V, int i, int cx, int cy, int k, double ray_k, double* nd, int* ni) {
+  const double xi = V.pts[3 * i], yi = V.pts[3 * i + 1], zi = V.pts[3 * i + 2];
+  int cnt = 0;
+  double worst = CUDART_INF;
+  int worst_j = 0x7fffffff;
+  const int wmax = max(max(cx, V.w - 1 - cx), max(cy, V.h - 1 - cy));
+  for (int w = 0; w <= wmax; ++w) {
+    const int y0 = cy - w, y1 = cy + w, x0 = cx - w, x1 = cx + w;
+    for (int y = max(y0, 0); y <= min(y1, V.h - 1); ++y) {
+      const bool edge_row = (y == y0 || y == y1);
+      const int step = edge_row ? 1 : max(2 * w, 1);
+      for (int x = x0; x <= x1; x += step) {
+        if (x < 0 || x >= V.w) continue;
+        const int j = V.map[y * V.w + x];
+        if (j < 0) continue;
+        const double dx = V.pts[3 * j] - xi, dy = V.pts[3 * j + 1] - yi, dz = V.pts[3 * j + 2] - zi;
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        int pos;
+        if (cnt < k)
+          pos = cnt++;
+        else if (d2 < worst || (d2 == worst && j < worst_j))
+          pos = k - 1;
+        else
+          continue;
+        while (pos > 0 && (nd[pos - 1] > d2 || (nd[pos - 1] == d2 && ni[pos - 1] > j))) nd[pos] = nd[pos - 1], ni[pos] = ni[pos - 1], --pos;
+        nd[pos] = d2, ni[pos] = j;
+        if (cnt == k) worst = nd[k - 1], worst_j = ni[k - 1];
+      }
+    }
+    if (cnt == k) {
+      const double D = zi * (double)(w + 1) * ray_k;
+      if (worst < D * D) break;
+    }
+  }
+}
+
+// mean / covariance / Jacobi / regularised output for a sorted neighbour list
+// (registration.py:143-216)
+__device__ __forceinline__ void cov_from_neighbours(const double* __restrict__ pts, const int* ni, int k, double eps,
+                                                    double* __restrict__ out) {
+  double mx = 0.0, my = 0.0, mz = 0.0;
+  for (int q = 0; q < k; ++q) mx += pts[3 * ni[q]], my += pts[3 * ni[q] + 1], mz += pts[3 * ni[q] + 2];
+  const double kd = (double)k;
+  mx /= kd, my /= kd, mz /= kd;
+  double a00 = 0, a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0;
+  for (int q = 0; q < k; ++q) {
+    const double dx = pts[3 * ni[q]] - mx, dy = pts[3 * ni[q] + 1] - my, dz = pts[3 * ni[q] + 2] - mz;
+    a00 += dx * dx, a01 += dx * dy, a02 += dx * dz, a11 += dy * dy, a12 += dy * dz, a22 += dz * dz;
+  }
+  double a[3][3], vm[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  a[0][0] = a00 / kd, a[0][1] = a01 / kd, a[0][2] = a02 / kd;
+  a[1][1] = a11 / kd, a[1][2] = a12 / kd, a[2][2] = a22 / kd;
+  a[1][0] = a[0][1], a[2][0] = a[0][2], a[2][1] = a[1][2];
+  for (int sweep = 0; sweep < 16; ++sweep) {
+    const double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+    const double scale = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]) + 1e-300;
+    if (off <= 1e-14 * scale) break;
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int q = p + 1; q < 3; ++q) {
+        const double apq = a[p][q];
+        if (apq == 0.0) continue;
+        const double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+        double tt;
+        if (theta >= 0.0)
+          tt = 1.0 / (theta + sqrt(theta * theta + 1.0));
+        else
+          tt = -1.0 / (-theta + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double tmp = a[r][p];
+          a[r][p] = c * tmp - s * a[r][q];
+          a[r][q] = s * tmp + c * a[r][q];
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double tmp = a[p][r];
+          a[p][r] = c * tmp - s * a[q][r];
+          a[q][r] = s * tmp + c * a[q][r];
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const double tmp = vm[r][p];
+          vm[r][p] = c * tmp - s * vm[r][q];
+          vm[r][q] = s * tmp + c * vm[r][q];
+        }
+      }
+  }
+  double dmin = a[0][0], x = vm[0][0], y = vm[1][0], z = vm[2][0];
+  if (a[1][1] < dmin) dmin = a[1][1], x = vm[0][1], y = vm[1][1], z = vm[2][1];
+  if (a[2][2] < dmin) dmin = a[2][2], x = vm[0][2], y = vm[1][2], z = vm[2][2];
+  const double f = 1.0 - eps;
+  out[0] = 1.0 - f * x * x, out[1] = -f * x * y, out[2] = -f * x * z;
+  out[3] = out[1], out[4] = 1.0 - f * y * y, out[5] = -f * y * z;
+  out[6] = out[2], out[7] = out[5], out[8] = 1.0 - f * z * z;
+}
+
+__device__ void cov_point_org(const OrgView& V, int i, int cx, int cy, int k, double eps, double ray_k, double* __restrict__ out) {
+  double nd[PX_KCOV_MAX];
+  int ni[PX_KCOV_MAX];
+  knn_ring(V, i, cx, cy, k, ray_k, nd, ni);
+  cov_from_neighbours(V.pts, ni, k, eps, out);
+}
+
+// one CTA per target cloud, threads over its points
 __global__ void __launch_bounds__(128) cov_kernel(CovArgs a) {
   const int c = blockIdx.x;
   const long long off = a.offset[c];
   const int n = a.count ? a.count[c] : (int)(a.offset[c + 1] - off);
   if (n <= a.k) return;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) cov_point(a.points + 3 * off, n, i, a.k, a.eps, a.cov + 9 * (off + i));
+  const bool org = a.org != nullptr && a.org[c].w > 0;
+  if (org) {
+    const TgtOrg o = a.org[c];
+    OrgView V{a.points + 3 * off, a.tmap + o.map_off, o.w, o.h};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int cell = a.tpix[off + i];
+      cov_point_org(V, i, cell % o.w, cell / o.w, a.k, a.eps, a.ray_k, a.cov + 9 * (off + i));
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) cov_point(a.points + 3 * off, n, i, a.k, a.eps, a.cov + 9 * (off + i));
+  }
 }
 
 cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
@@ -118,6 +256,148 @@ cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
+// Per-target "anything within the gate?" bits: occupancy of a coarse 3-D grid over
+// the padded AABB, dilated by rd cells (Chebyshev).  A query whose cell bit is 0
+// has no target point within the gate, exactly.
+
+__device__ __forceinline__ int grid_cell(double x, double o, double inv_h) { return (int)floor((x - o) * inv_h); }
+
+__global__ void __launch_bounds__(256) target_near_kernel(NearBuildArgs a) {
+  extern __shared__ unsigned char nsm[];  // occ0[ncell] | occ1[ncell]
+  const int t = blockIdx.x;
+  const TgtNear g = a.near[t];
+  const long long off = a.offset[t];
+  const int n = (int)(a.offset[t + 1] - off);
+  const int ncell = g.nx * g.ny * g.nz;
+  unsigned char* occ0 = nsm;
+  unsigned char* occ1 = nsm + ncell;
+  const double* P = a.points + 3 * off;
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) occ0[c] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int cx = grid_cell(P[3 * i], g.ox, g.inv_h), cy = grid_cell(P[3 * i + 1], g.oy, g.inv_h),
+              cz = grid_cell(P[3 * i + 2], g.oz, g.inv_h);
+    occ0[(cz * g.ny + cy) * g.nx + cx] = 1;
+  }
+  for (int pass = 0; pass < 3; ++pass) {
+    __syncthreads();
+    const unsigned char* in = (pass & 1) ? occ1 : occ0;
+    unsigned char* out = (pass & 1) ? occ0 : occ1;
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+      const int cx = c % g.nx, cy = (c / g.nx) % g.ny, cz = c / (g.nx * g.ny);
+      int stride, pos, len;
+      if (pass == 0) stride = 1, pos = cx, len = g.nx;
+      else if (pass == 1) stride = g.nx, pos = cy, len = g.ny;
+      else stride = g.nx * g.ny, pos = cz, len = g.nz;
+      unsigned char v = 0;
+      const int a0 = max(0, pos - g.rd), a1 = min(len - 1, pos + g.rd);
+      for (int q = a0; q <= a1 && !v; ++q) v = in[c + (q - pos) * stride];
+      out[c] = v;
+    }
+  }
+  __syncthreads();
+  const unsigned char* fin = occ1;  // occ0 -> occ1 -> occ0 -> occ1
+  uint32_t* nb = a.near_bits + g.bit_off;
+  for (int w = threadIdx.x; w < (ncell + 31) / 32; w += blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32 && 32 * w + b < ncell; ++b) bits |= (uint32_t)(fin[32 * w + b] != 0) << b;
+    nb[w] = bits;
+  }
+}
+
+cudaError_t launch_target_near(const NearBuildArgs& a, cudaStream_t st) {
+  if (a.n_targets == 0) return cudaSuccess;
+  const size_t smem = 2 * PX_GRID_MAX_CELLS + 16;
+  cudaError_t e = cudaFuncSetAttribute(target_near_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  target_near_kernel<<<a.n_targets, 256, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Exact nearest neighbour of q among one target's points: the lexicographic
+// minimum of (d2, index), identical to the reference's brute-force scan
+// (registration.py:251-260) whenever that minimum passes the gate; bj = -1 or
+// best > gate2 otherwise.  `prev` is last iteration's correspondence: its current
+// distance bounds the pixel window that has to be searched.
+__device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long toff, int nt, const Camera& cam,
+                                          double qx, double qy, double qz, int prev, double gate2, double& best, int& bj) {
+  best = CUDART_INF, bj = -1;
+  const double* P = T.points + 3 * toff;
+  const TgtOrg o = T.org ? T.org[ti] : TgtOrg{0, 0, 0, 0, 0};
+  if (o.w > 0 && qz > 1e-3) {
+    double ub = gate2;
+    bool bounded = false;
+    if (prev >= 0) {
+      const double dx = P[3 * prev] - qx, dy = P[3 * prev + 1] - qy, dz = P[3 * prev + 2] - qz;
+      const double d2 = dx * dx + dy * dy + dz * dz;
+      if (d2 <= ub) ub = d2, bounded = true;
+    }
+    if (!bounded) {
+      const TgtNear g = T.near[ti];
+      const int cx = grid_cell(qx, g.ox, g.inv_h), cy = grid_cell(qy, g.oy, g.inv_h), cz = grid_cell(qz, g.oz, g.inv_h);
+      if (!(cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny && cz >= 0 && cz < g.nz)) return;  // beyond the padded AABB
+      const int c = (cz * g.ny + cy) * g.nx + cx;
+      if (!((T.near_bits[g.bit_off + (c >> 5)] >> (c & 31)) & 1u)) return;
+    }
+    const int32_t* map = T.tmap + o.map_off;
+    const int st = cam.stride;
+    const double uq = cam.fx * qx / qz + cam.cx, vq = cam.fy * qy / qz + cam.cy;
+    const double rho = sqrt(ub);
+    if (bounded && qz > rho + 1e-3) {
+      // every point within rho of q projects inside this window (see px_cost.cu)
+      const double zr = qz - rho;
+      const double ru = cam.fx * rho * (1.0 + fabs(qx / qz)) / zr + 1e-6;
+      const double rv = cam.fy * rho * (1.0 + fabs(qy / qz)) / zr + 1e-6;
+      int x0 = (int)ceil((uq - ru - 0.5) / st) - o.gx0, x1 = (int)floor((uq + ru - 0.5) / st) - o.gx0;
+      int y0 = (int)ceil((vq - rv - 0.5) / st) - o.gy0, y1 = (int)floor((vq + rv - 0.5) / st) - o.gy0;
+      x0 = max(x0, 0), y0 = max(y0, 0), x1 = min(x1, o.w - 1), y1 = min(y1, o.h - 1);
+      for (int y = y0; y <= y1; ++y)
+        for (int x = x0; x <= x1; ++x) {
+          const int j = map[y * o.w + x];
+          if (j < 0) continue;
+          const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
+          const double d2 = dx * dx + dy * dy + dz * dz;
+          if (d2 < best) best = d2, bj = j;  // row-major scan == ascending index
+        }
+      return;
+    }
+    // unbounded: rings around q's pixel until the bound beats the best or the gate
+    const double fcx = floor((uq - 0.5) / st + 0.5), fcy = floor((vq - 0.5) / st + 0.5);
+    if (fabs(fcx) < 1e8 && fabs(fcy) < 1e8) {
+      const int cx = (int)fcx - o.gx0, cy = (int)fcy - o.gy0;
+      // rings that cannot intersect the map are skipped; beyond wmax nothing is left
+      const int wmin = max(max(-cx, cx - (o.w - 1)), max(max(-cy, cy - (o.h - 1)), 0));
+      const int wmax = max(max(cx, o.w - 1 - cx), max(cy, o.h - 1 - cy));
+      for (int w = wmin; w <= wmax; ++w) {
+        if (w > 0) {  // lower bound for everything on ring >= w
+          const double D = qz * ((double)w - 0.5) * cam.ray_k;
+          const double D2 = D * D;
+          if (best < D2 || D2 > gate2) break;
+        }
+        const int y0 = cy - w, y1 = cy + w, x0 = cx - w, x1 = cx + w;
+        for (int y = max(y0, 0); y <= min(y1, o.h - 1); ++y) {
+          const bool edge_row = (y == y0 || y == y1);
+          const int step = edge_row ? 1 : max(2 * w, 1);
+          for (int x = x0; x <= x1; x += step) {
+            if (x < 0 || x >= o.w) continue;
+            const int j = map[y * o.w + x];
+            if (j < 0) continue;
+            const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j;
+          }
+        }
+      }
+      return;
+    }
+  }
+  // generic clouds / degenerate projection: the reference's linear scan
+  for (int j = 0; j < nt; ++j) {
+    const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
+    const double d2 = dx * dx + dy * dy + dz * dz;
+    if (d2 < best) best = d2, bj = j;
+  }
+}
 
 #define STAGE_LD 33
 #define WARP_SM_DOUBLES (43 * STAGE_LD + 43 + 8)
@@ -292,7 +572,16 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs 
   if (n <= cfg.k_cov || nt <= cfg.k_cov) {
     failure = F_TOO_FEW;  // registration.py:504-510
   } else {
-    for (int i = lane; i < n; i += 32) cov_point(src, n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
+    if (a.src.slot_map) {
+      const int4 bb = a.src.bbox[c];
+      OrgView V{src, a.src.slot_map + off, bb.z, bb.w};
+      const int32_t* spx = a.src.src_px + 2 * off;
+      const int st = a.cam.stride;
+      for (int i = lane; i < n; i += 32)
+        cov_point_org(V, i, spx[2 * i] / st - bb.x, spx[2 * i + 1] / st - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k, ca + 9 * (size_t)i);
+    } else {
+      for (int i = lane; i < n; i += 32) cov_point(src, n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
+    }
     __syncwarp();
     double r_try[9], t_try[3];
     for (int it = 1; it <= cfg.max_iter; ++it) {
@@ -308,14 +597,9 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs 
           const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
           const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
           const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
-          double best = CUDART_INF;
-          int bj = -1;
-#pragma unroll 4
-          for (int j = 0; j < nt; ++j) {
-            const double dx = tgt[3 * j] - px, dy = tgt[3 * j + 1] - py, dz = tgt[3 * j + 2] - pz;
-            const double d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < best) best = d2, bj = j;
-          }
+          double best;
+          int bj;
+          nn_target(a.tgt, ti, toff, nt, a.cam, px, py, pz, it == 1 ? -1 : corr[i], cfg.gate2, best, bj);
           int cj = -1;
           if (bj >= 0 && !(best > cfg.gate2)) {
             const double* cai = ca + 9 * (size_t)i;

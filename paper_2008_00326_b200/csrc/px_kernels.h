@@ -44,6 +44,7 @@ struct RenderArgs {
   double* points;             // (sum cap,3)
   double* lab;                // (sum cap,3)
   int32_t* src_px;            // (sum cap,2)
+  int32_t* slot_map;          // (sum cap) out: compact index of every screen-box slot, -1 = empty
   // dense single-view output (px_rasterize)
   double* dense_z;
   double* dense_c;
@@ -70,6 +71,25 @@ struct CloudsDev {
   const double* points;
   const double* lab;
   const int32_t* src_px;
+  const int32_t* slot_map;  // (sum cap) compact index per screen-box slot or -1; null for uploaded clouds
+  const int4* bbox;         // (n) screen box (gu_lo, gv_lo, gw, gh); null for uploaded clouds
+};
+
+// "Anything within the gate?" bits over a coarse 3-D grid covering one target's
+// AABB grown by pad >= gate (see px_gicp.cu).
+struct TgtNear {
+  double ox, oy, oz, inv_h;
+  int nx, ny, nz;
+  int rd;              // dilation radius in cells: floor(gate/h)+1
+  long long bit_off;   // into near_bits (32-bit words)
+};
+
+// Organised view of one target: its points are observed-cloud points, i.e. they
+// sit on stride-grid pixels of the frame.  map[(gy-gy0)*w + (gx-gx0)] = local
+// index or -1.  w == 0: not organised (generic cloud) -> linear scans.
+struct TgtOrg {
+  int gx0, gy0, w, h;
+  long long map_off;
 };
 
 struct TargetsDev {
@@ -77,7 +97,21 @@ struct TargetsDev {
   const long long* offset;  // (n_targets+1)
   const double* points;     // (sum,3)
   const double* cov;        // (sum,9)
+  const TgtNear* near;      // (n_targets)
+  const uint32_t* near_bits;
+  const TgtOrg* org;        // (n_targets) or null
+  const int32_t* tmap;
 };
+
+#define PX_GRID_MAX_CELLS 32768
+struct NearBuildArgs {
+  int n_targets;
+  const long long* offset;
+  const double* points;
+  const TgtNear* near;
+  uint32_t* near_bits;
+};
+cudaError_t launch_target_near(const NearBuildArgs& a, cudaStream_t st);
 
 struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   int n_clouds;
@@ -87,6 +121,11 @@ struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   double* cov;              // (sum,9)
   int k;
   double eps;
+  // organised targets (nullable): ring search instead of the linear scan
+  const TgtOrg* org;
+  const int32_t* tmap;
+  const int32_t* tpix;      // (sum) map cell (y*w+x) of every target point
+  double ray_k;
 };
 cudaError_t launch_cov(const CovArgs& a, long long total_points, cudaStream_t st);
 
@@ -96,6 +135,7 @@ struct RefineArgs {
   const int32_t* target_idx;  // (n)
   const double* init_T;       // (n,12) or null = identity
   GicpCfgDev cfg;
+  Camera cam;
   // scratch, indexed by the source slot offsets
   double* src_cov;            // (sum cap,9)
   double* w_buf;              // (sum cap,9)

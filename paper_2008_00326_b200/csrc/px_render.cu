@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(PX_RENDER_THREADS) render_kernel(RenderArgs a)
         cg = s0 * k0[1] + s1 * k1[1] + s2 * k2[1];
         cb = s0 * k0[2] + s1 * k1[2] + s2 * k2[2];
       }
+      if (!DENSE && li < npix) a.slot_map[out0 + (long long)r0 * gw + li] = -1;
       if (DENSE) {
         if (have) {
           const size_t o = (size_t)py * cam.W + px;
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(PX_RENDER_THREADS) render_kernel(RenderArgs a)
         srgb_to_lab(srgb_encode1(cr), srgb_encode1(cg), srgb_encode1(cb), L, A, B);
         a.lab[3 * o] = L, a.lab[3 * o + 1] = A, a.lab[3 * o + 2] = B;
         a.src_px[2 * o] = px, a.src_px[2 * o + 1] = py;
+        a.slot_map[out0 + (long long)r0 * gw + li] = pos;
       }
       __syncthreads();
       if (tid == 0) s_base += chunk_total;

@@ -198,11 +198,13 @@ class Engine:
         N.check(self.ctx, rc, "px_covariances")
         return out
 
-    def upload_targets(self, offsets, points, k, eps):
+    def upload_targets(self, offsets, points, gicp_cfg, obs_index=None):
         offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         points = N.f64(points)
+        oi = None if obs_index is None else np.ascontiguousarray(obs_index, dtype=np.int64)
+        g = self._gicp_cfg(gicp_cfg)
         rc = self.lib.px_targets_upload(self.ctx, offsets.shape[0] - 1, N.ptr(offsets, N.i64p), N.ptr(points, N.f64p),
-                                        int(k), float(eps))
+                                        N.ptr(oi, N.i64p), C.byref(g))
         N.check(self.ctx, rc, "px_targets_upload")
 
     def target_covariances(self, total) -> np.ndarray:
@@ -234,7 +236,7 @@ class Engine:
         offs = np.zeros(len(targets) + 1, dtype=np.int64)
         np.cumsum([t.shape[0] for t in targets], out=offs[1:])
         tp = np.concatenate(targets) if targets else np.zeros((0, 3))
-        self.upload_targets(offs, tp, cfg.k_covariance, cfg.epsilon)
+        self.upload_targets(offs, tp, cfg)
         if not sources:
             return []
         h = self._upload_clouds(sources)
@@ -351,8 +353,7 @@ class Engine:
         self.upload_scene(frame, plan.cfg.stride, plan.observed, plan.obs_labels)
         self.upload_models({oid: models[oid] for oid in plan.active})
         if plan.cfg.refine and plan.target_offsets is not None:
-            self.upload_targets(plan.target_offsets, plan.target_points, plan.cfg.gicp.k_covariance,
-                                plan.cfg.gicp.epsilon)
+            self.upload_targets(plan.target_offsets, plan.target_points, plan.cfg.gicp, plan.target_obs_index)
 
     def run_plan(self, frame, models, plan, index=None):
         """Scene/model/target upload + fused search for the plan's candidates."""

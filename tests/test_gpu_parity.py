@@ -193,7 +193,8 @@ def test_target_covariances_bit_exact(engine, name):
     d, frame, models, cfg, plan = G.scene(name)
     if not cfg.refine:
         pytest.skip("no refine")
-    engine.upload_targets(plan.target_offsets, plan.target_points, cfg.gicp.k_covariance, cfg.gicp.epsilon)
+    engine.upload_scene(frame, cfg.stride, plan.observed, plan.obs_labels)
+    engine.upload_targets(plan.target_offsets, plan.target_points, cfg.gicp, plan.target_obs_index)
     cov = engine.target_covariances(int(plan.target_offsets[-1]))
     for t in range(0, len(plan.target_offsets) - 1, max(1, (len(plan.target_offsets) - 1) // 12)):
         a, b = int(plan.target_offsets[t]), int(plan.target_offsets[t + 1])
@@ -299,3 +300,37 @@ def test_estimate_poses_public_entry(engine):
     assert res.proposals_evaluated == ref["proposals_evaluated"] and res.observed_points == int(d["n_obs"])
     for e, r in zip(res.estimates, ref["objects"]):
         assert (e.object_id, e.proposal_index, e.cost.j_o, e.cost.j_r) == (r["object_id"], r["proposal_index"], r["j_o"], r["j_r"])
+
+
+def test_organised_targets_equal_generic(engine):
+    """The organised (pixel-ring) neighbour searches are exact: refining the same
+    rendered clouds against targets uploaded with and without their
+    observed-cloud indices gives bit-identical transforms, and so do the
+    covariances."""
+    d, frame, models, cfg, plan = G.scene("c3_clutter_3dof")
+    engine.upload_scene(frame, cfg.stride, plan.observed, plan.obs_labels)
+    engine.upload_models(models)
+    sel = np.arange(0, plan.n, 7)
+    h = engine.render_clouds_handle(plan.flat_oid[sel], plan.cam_poses[sel], cfg.occluder_marking, cfg.delta)
+    try:
+        clouds = engine._download_clouds(h)
+        engine.upload_targets(plan.target_offsets, plan.target_points, cfg.gicp, plan.target_obs_index)
+        cov_o = engine.target_covariances(int(plan.target_offsets[-1]))
+        To, ito, flo, *_ = engine.refine_handle(h, plan.target_idx[sel], cfg.gicp)
+        engine.upload_targets(plan.target_offsets, plan.target_points, cfg.gicp, None)
+        cov_g = engine.target_covariances(int(plan.target_offsets[-1]))
+        Tg, itg, flg, *_ = engine.refine_handle(h, plan.target_idx[sel], cfg.gicp)
+    finally:
+        engine.lib.px_clouds_free(engine.ctx, h)
+    sizes = np.diff(plan.target_offsets)
+    big = np.repeat(sizes > cfg.gicp.k_covariance, sizes)
+    assert np.array_equal(cov_o[big], cov_g[big])
+    assert np.array_equal(ito, itg) and np.array_equal(flo, flg)
+    assert np.array_equal(To, Tg)
+    # and uploaded (generic) source clouds behave like device-rendered ones
+    hu = engine._upload_clouds([c.points for c in clouds])
+    try:
+        Tu, itu, flu, *_ = engine.refine_handle(hu, plan.target_idx[sel], cfg.gicp)
+    finally:
+        engine.lib.px_clouds_free(engine.ctx, hu)
+    assert np.array_equal(Tu, Tg) and np.array_equal(itu, itg)
