@@ -82,7 +82,7 @@ struct px_ctx {
   long long tgt_total = 0;
   int tgt_k = 0;
   double tgt_gate = 0.0;
-  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_near, tgt_bits, tgt_org, tgt_map, tgt_pix;
+  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_org, tgt_map, tgt_pix, tgt_boxes;
   bool tgt_organised = false;
   // resident candidates
   int64_t n_cand = 0;
@@ -325,7 +325,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
-                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_near, &ctx->tgt_bits, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
+                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
@@ -662,10 +662,9 @@ static TargetsDev targets_dev(px_ctx* ctx) {
   t.offset = ctx->tgt_off.as<long long>();
   t.points = ctx->tgt_pts.as<double>();
   t.cov = ctx->tgt_cov.as<double>();
-  t.near = ctx->tgt_near.as<TgtNear>();
-  t.near_bits = ctx->tgt_bits.as<uint32_t>();
   t.org = ctx->tgt_organised ? ctx->tgt_org.as<TgtOrg>() : nullptr;
   t.tmap = ctx->tgt_map.as<int32_t>();
+  t.boxes = ctx->tgt_boxes.as<double>();
   return t;
 }
 
@@ -685,46 +684,19 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   std::vector<long long> off((size_t)n_targets + 1, 0);
   for (int i = 0; i <= n_targets && n_targets; ++i) off[(size_t)i] = (long long)offsets[i];
 
-  // (1) near-bit grids: AABB grown by pad >= gate, cell h = gate/8 coarsened to the cell budget
-  std::vector<TgtNear> nears((size_t)n_targets);
-  long long word_total = 0;
-  const double pad = gate * (1.0 + 1e-6) + 1e-9;
-  for (int t = 0; t < n_targets; ++t) {
-    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    const long long a = off[(size_t)t], b = off[(size_t)t + 1];
-    for (long long i = a; i < b; ++i)
-      for (int d = 0; d < 3; ++d) {
-        const double v = points[3 * i + d];
-        if (!std::isfinite(v)) return fail(ctx, PX_E_ARG, "non-finite target point");
-        if (i == a || v < lo[d]) lo[d] = v;
-        if (i == a || v > hi[d]) hi[d] = v;
-      }
-    double h = gate / 8.0;
-    int nx, ny, nz;
-    for (;;) {
-      nx = (int)std::floor((hi[0] - lo[0] + 2 * pad) / h) + 2;
-      ny = (int)std::floor((hi[1] - lo[1] + 2 * pad) / h) + 2;
-      nz = (int)std::floor((hi[2] - lo[2] + 2 * pad) / h) + 2;
-      if ((long long)nx * ny * nz <= PX_GRID_MAX_CELLS) break;
-      h *= 1.1;
-    }
-    TgtNear& g = nears[(size_t)t];
-    g.ox = lo[0] - pad, g.oy = lo[1] - pad, g.oz = lo[2] - pad, g.inv_h = 1.0 / h;
-    g.nx = nx, g.ny = ny, g.nz = nz;
-    g.rd = (int)std::floor(gate / h) + 1;
-    g.bit_off = word_total;
-    word_total += ((long long)nx * ny * nz + 31) / 32;
-  }
+  for (long long i = 0; i < 3 * total; ++i)
+    if (!std::isfinite(points[i])) return fail(ctx, PX_E_ARG, "non-finite target point");
 
-  // (2) organised views: valid when every target is an index-ascending subset of the
+  // organised views: valid when every target is an index-ascending subset of the
   // uploaded scene's organised observed cloud
   bool org = obs_index != nullptr && ctx->have_scene && ctx->organised && !ctx->h_obs_src.empty();
   std::vector<TgtOrg> orgs((size_t)n_targets);
   std::vector<int32_t> tmap, tpix;
+  std::vector<double> boxes;
   if (org) {
     const int st = ctx->cam.stride;
     tpix.resize((size_t)total);
-    long long map_total = 0;
+    long long map_total = 0, box_total = 0;
     for (int t = 0; t < n_targets && org; ++t) {
       const long long a = off[(size_t)t], b = off[(size_t)t + 1];
       int x0 = 1 << 30, y0 = 1 << 30, x1 = -1, y1 = -1;
@@ -742,19 +714,36 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
       TgtOrg& o = orgs[(size_t)t];
       if (b > a) o.gx0 = x0, o.gy0 = y0, o.w = x1 - x0 + 1, o.h = y1 - y0 + 1;
       else o.gx0 = o.gy0 = 0, o.w = 1, o.h = 1;
-      o.map_off = map_total;
+      o.bw = (o.w + PX_BLK - 1) / PX_BLK, o.bh = (o.h + PX_BLK - 1) / PX_BLK;
+      o.sw = (o.bw + PX_BLK - 1) / PX_BLK, o.sh = (o.bh + PX_BLK - 1) / PX_BLK;
+      o.map_off = map_total, o.box_off = box_total;
       map_total += (long long)o.w * o.h;
+      box_total += (long long)o.bw * o.bh + (long long)o.sw * o.sh;
     }
     if (org) {
       tmap.assign((size_t)map_total, -1);
+      boxes.resize((size_t)box_total * 6);
+      for (long long q = 0; q < box_total; ++q)
+        for (int d = 0; d < 3; ++d) boxes[(size_t)(6 * q + d)] = INFINITY, boxes[(size_t)(6 * q + 3 + d)] = -INFINITY;
       for (int t = 0; t < n_targets; ++t) {
         const TgtOrg& o = orgs[(size_t)t];
         const long long a = off[(size_t)t], b = off[(size_t)t + 1];
+        double* bb = boxes.data() + 6 * o.box_off;
+        double* sb = bb + 6 * (long long)o.bw * o.bh;
         for (long long i = a; i < b; ++i) {
           const long long oi = obs_index[i];
-          const int cell = (ctx->h_obs_src[2 * oi + 1] / st - o.gy0) * o.w + (ctx->h_obs_src[2 * oi] / st - o.gx0);
+          const int x = ctx->h_obs_src[2 * oi] / st - o.gx0, y = ctx->h_obs_src[2 * oi + 1] / st - o.gy0;
+          const int cell = y * o.w + x;
           tmap[(size_t)(o.map_off + cell)] = (int32_t)(i - a);
           tpix[(size_t)i] = cell;
+          double* nb[2] = {bb + 6 * ((y / PX_BLK) * o.bw + x / PX_BLK),
+                           sb + 6 * ((y / (PX_BLK * PX_BLK)) * o.sw + x / (PX_BLK * PX_BLK))};
+          for (double* n6 : nb)
+            for (int d = 0; d < 3; ++d) {
+              const double v = points[3 * i + d];
+              if (v < n6[d]) n6[d] = v;
+              if (v > n6[3 + d]) n6[3 + d] = v;
+            }
         }
       }
     }
@@ -763,15 +752,14 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
 
   if (int r = h2d(ctx, ctx->tgt_off, off.data(), off.size() * 8)) return r;
   if (int r = h2d(ctx, ctx->tgt_pts, points, (size_t)total * 24)) return r;
-  if (int r = h2d(ctx, ctx->tgt_near, nears.data(), nears.size() * sizeof(TgtNear))) return r;
   if (org) {
     if (int r = h2d(ctx, ctx->tgt_org, orgs.data(), orgs.size() * sizeof(TgtOrg))) return r;
     if (int r = h2d(ctx, ctx->tgt_map, tmap.data(), tmap.size() * 4)) return r;
     if (int r = h2d(ctx, ctx->tgt_pix, tpix.data(), tpix.size() * 4)) return r;
+    if (int r = h2d(ctx, ctx->tgt_boxes, boxes.data(), boxes.size() * 8)) return r;
   }
   const size_t tot1 = (size_t)std::max<long long>(total, 1);
   CU(ctx->tgt_cov.ensure(tot1 * 72));
-  CU(ctx->tgt_bits.ensure((size_t)std::max<long long>(word_total, 1) * 4));
   ctx->n_targets = n_targets, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = gate;
   if (n_targets) {
     CovArgs a{};
@@ -780,10 +768,7 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     if (org) a.org = ctx->tgt_org.as<TgtOrg>(), a.tmap = ctx->tgt_map.as<int32_t>(), a.tpix = ctx->tgt_pix.as<int32_t>();
     a.ray_k = ctx->cam.ray_k;
     CU(launch_cov(a, total, ctx->stream));
-    NearBuildArgs nb{n_targets, ctx->tgt_off.as<long long>(), ctx->tgt_pts.as<double>(), ctx->tgt_near.as<TgtNear>(),
-                     ctx->tgt_bits.as<uint32_t>()};
-    CU(launch_target_near(nb, ctx->stream));
-    ctx->launches += 2;
+    ctx->launches += 1;
   }
   CU(cudaStreamSynchronize(ctx->stream));  // host staging vectors are stack-owned
   return 0;

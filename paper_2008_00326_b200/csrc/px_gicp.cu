@@ -256,142 +256,67 @@ cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// Per-target "anything within the gate?" bits: occupancy of a coarse 3-D grid over
-// the padded AABB, dilated by rd cells (Chebyshev).  A query whose cell bit is 0
-// has no target point within the gate, exactly.
+// Exact nearest neighbour over an organised target with a two-level box
+// hierarchy in image space: blocks of PX_BLK x PX_BLK map cells and super-blocks
+// of PX_BLK x PX_BLK blocks, each with the 3-D bounding box of its points.  A
+// node is opened only if the squared distance from the query to its box is <=
+// the current cut-off; that box distance, evaluated with the same operation
+// order as the point distance, can never exceed the point distance of any
+// member (floating-point subtraction, multiplication and addition are
+// monotone), so no candidate is ever skipped.
 
-__device__ __forceinline__ int grid_cell(double x, double o, double inv_h) { return (int)floor((x - o) * inv_h); }
-
-__global__ void __launch_bounds__(256) target_near_kernel(NearBuildArgs a) {
-  extern __shared__ unsigned char nsm[];  // occ0[ncell] | occ1[ncell]
-  const int t = blockIdx.x;
-  const TgtNear g = a.near[t];
-  const long long off = a.offset[t];
-  const int n = (int)(a.offset[t + 1] - off);
-  const int ncell = g.nx * g.ny * g.nz;
-  unsigned char* occ0 = nsm;
-  unsigned char* occ1 = nsm + ncell;
-  const double* P = a.points + 3 * off;
-  for (int c = threadIdx.x; c < ncell; c += blockDim.x) occ0[c] = 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int cx = grid_cell(P[3 * i], g.ox, g.inv_h), cy = grid_cell(P[3 * i + 1], g.oy, g.inv_h),
-              cz = grid_cell(P[3 * i + 2], g.oz, g.inv_h);
-    occ0[(cz * g.ny + cy) * g.nx + cx] = 1;
-  }
-  for (int pass = 0; pass < 3; ++pass) {
-    __syncthreads();
-    const unsigned char* in = (pass & 1) ? occ1 : occ0;
-    unsigned char* out = (pass & 1) ? occ0 : occ1;
-    for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
-      const int cx = c % g.nx, cy = (c / g.nx) % g.ny, cz = c / (g.nx * g.ny);
-      int stride, pos, len;
-      if (pass == 0) stride = 1, pos = cx, len = g.nx;
-      else if (pass == 1) stride = g.nx, pos = cy, len = g.ny;
-      else stride = g.nx * g.ny, pos = cz, len = g.nz;
-      unsigned char v = 0;
-      const int a0 = max(0, pos - g.rd), a1 = min(len - 1, pos + g.rd);
-      for (int q = a0; q <= a1 && !v; ++q) v = in[c + (q - pos) * stride];
-      out[c] = v;
-    }
-  }
-  __syncthreads();
-  const unsigned char* fin = occ1;  // occ0 -> occ1 -> occ0 -> occ1
-  uint32_t* nb = a.near_bits + g.bit_off;
-  for (int w = threadIdx.x; w < (ncell + 31) / 32; w += blockDim.x) {
-    uint32_t bits = 0;
-    for (int b = 0; b < 32 && 32 * w + b < ncell; ++b) bits |= (uint32_t)(fin[32 * w + b] != 0) << b;
-    nb[w] = bits;
-  }
+__device__ __forceinline__ double box_dist2(const double* __restrict__ b, double qx, double qy, double qz) {
+  // b = {xlo, ylo, zlo, xhi, yhi, zhi}; empty boxes hold +inf / -inf and give +inf
+  const double dx = fmax(fmax(b[0] - qx, qx - b[3]), 0.0);
+  const double dy = fmax(fmax(b[1] - qy, qy - b[4]), 0.0);
+  const double dz = fmax(fmax(b[2] - qz, qz - b[5]), 0.0);
+  return dx * dx + dy * dy + dz * dz;
 }
 
-cudaError_t launch_target_near(const NearBuildArgs& a, cudaStream_t st) {
-  if (a.n_targets == 0) return cudaSuccess;
-  const size_t smem = 2 * PX_GRID_MAX_CELLS + 16;
-  cudaError_t e = cudaFuncSetAttribute(target_near_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  target_near_kernel<<<a.n_targets, 256, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-// Exact nearest neighbour of q among one target's points: the lexicographic
-// minimum of (d2, index), identical to the reference's brute-force scan
-// (registration.py:251-260) whenever that minimum passes the gate; bj = -1 or
-// best > gate2 otherwise.  `prev` is last iteration's correspondence: its current
-// distance bounds the pixel window that has to be searched.
-__device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long toff, int nt, const Camera& cam,
-                                          double qx, double qy, double qz, int prev, double gate2, double& best, int& bj) {
+// Lexicographic minimum of (d2, index) over the target points with d2 <= gate2,
+// identical to the reference's brute-force scan (registration.py:251-260)
+// whenever that scan's winner passes the gate; bj = -1 if no point is within the
+// gate.  `prev` (last iteration's correspondence, or -1) seeds the cut-off.
+__device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long toff, int nt, double qx, double qy,
+                                          double qz, int prev, double gate2, double& best, int& bj) {
   best = CUDART_INF, bj = -1;
   const double* P = T.points + 3 * toff;
-  const TgtOrg o = T.org ? T.org[ti] : TgtOrg{0, 0, 0, 0, 0};
-  if (o.w > 0 && qz > 1e-3) {
-    double ub = gate2;
-    bool bounded = false;
+  const TgtOrg o = T.org ? T.org[ti] : TgtOrg{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (o.w > 0) {
+    double cut = gate2;
     if (prev >= 0) {
       const double dx = P[3 * prev] - qx, dy = P[3 * prev + 1] - qy, dz = P[3 * prev + 2] - qz;
       const double d2 = dx * dx + dy * dy + dz * dz;
-      if (d2 <= ub) ub = d2, bounded = true;
-    }
-    if (!bounded) {
-      const TgtNear g = T.near[ti];
-      const int cx = grid_cell(qx, g.ox, g.inv_h), cy = grid_cell(qy, g.oy, g.inv_h), cz = grid_cell(qz, g.oz, g.inv_h);
-      if (!(cx >= 0 && cx < g.nx && cy >= 0 && cy < g.ny && cz >= 0 && cz < g.nz)) return;  // beyond the padded AABB
-      const int c = (cz * g.ny + cy) * g.nx + cx;
-      if (!((T.near_bits[g.bit_off + (c >> 5)] >> (c & 31)) & 1u)) return;
+      if (d2 <= cut) best = d2, bj = prev, cut = d2;
     }
     const int32_t* map = T.tmap + o.map_off;
-    const int st = cam.stride;
-    const double uq = cam.fx * qx / qz + cam.cx, vq = cam.fy * qy / qz + cam.cy;
-    const double rho = sqrt(ub);
-    if (bounded && qz > rho + 1e-3) {
-      // every point within rho of q projects inside this window (see px_cost.cu)
-      const double zr = qz - rho;
-      const double ru = cam.fx * rho * (1.0 + fabs(qx / qz)) / zr + 1e-6;
-      const double rv = cam.fy * rho * (1.0 + fabs(qy / qz)) / zr + 1e-6;
-      int x0 = (int)ceil((uq - ru - 0.5) / st) - o.gx0, x1 = (int)floor((uq + ru - 0.5) / st) - o.gx0;
-      int y0 = (int)ceil((vq - rv - 0.5) / st) - o.gy0, y1 = (int)floor((vq + rv - 0.5) / st) - o.gy0;
-      x0 = max(x0, 0), y0 = max(y0, 0), x1 = min(x1, o.w - 1), y1 = min(y1, o.h - 1);
-      for (int y = y0; y <= y1; ++y)
-        for (int x = x0; x <= x1; ++x) {
-          const int j = map[y * o.w + x];
-          if (j < 0) continue;
-          const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
-          const double d2 = dx * dx + dy * dy + dz * dz;
-          if (d2 < best) best = d2, bj = j;  // row-major scan == ascending index
-        }
-      return;
-    }
-    // unbounded: rings around q's pixel until the bound beats the best or the gate
-    const double fcx = floor((uq - 0.5) / st + 0.5), fcy = floor((vq - 0.5) / st + 0.5);
-    if (fabs(fcx) < 1e8 && fabs(fcy) < 1e8) {
-      const int cx = (int)fcx - o.gx0, cy = (int)fcy - o.gy0;
-      // rings that cannot intersect the map are skipped; beyond wmax nothing is left
-      const int wmin = max(max(-cx, cx - (o.w - 1)), max(max(-cy, cy - (o.h - 1)), 0));
-      const int wmax = max(max(cx, o.w - 1 - cx), max(cy, o.h - 1 - cy));
-      for (int w = wmin; w <= wmax; ++w) {
-        if (w > 0) {  // lower bound for everything on ring >= w
-          const double D = qz * ((double)w - 0.5) * cam.ray_k;
-          const double D2 = D * D;
-          if (best < D2 || D2 > gate2) break;
-        }
-        const int y0 = cy - w, y1 = cy + w, x0 = cx - w, x1 = cx + w;
-        for (int y = max(y0, 0); y <= min(y1, o.h - 1); ++y) {
-          const bool edge_row = (y == y0 || y == y1);
-          const int step = edge_row ? 1 : max(2 * w, 1);
-          for (int x = x0; x <= x1; x += step) {
-            if (x < 0 || x >= o.w) continue;
-            const int j = map[y * o.w + x];
-            if (j < 0) continue;
-            const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
-            const double d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j;
+    const double* bb = T.boxes + 6 * o.box_off;          // blocks, row-major (bh x bw)
+    const double* sb = bb + 6 * (long long)o.bw * o.bh;  // super-blocks, row-major (sh x sw)
+    for (int sy = 0; sy < o.sh; ++sy)
+      for (int sx = 0; sx < o.sw; ++sx) {
+        if (box_dist2(sb + 6 * (sy * o.sw + sx), qx, qy, qz) > cut) continue;
+        const int by1 = min(o.bh, (sy + 1) * PX_BLK), bx1 = min(o.bw, (sx + 1) * PX_BLK);
+        for (int by = sy * PX_BLK; by < by1; ++by)
+          for (int bx = sx * PX_BLK; bx < bx1; ++bx) {
+            if (box_dist2(bb + 6 * (by * o.bw + bx), qx, qy, qz) > cut) continue;
+            const int y1 = min(o.h, (by + 1) * PX_BLK), x1 = min(o.w, (bx + 1) * PX_BLK);
+            for (int y = by * PX_BLK; y < y1; ++y)
+              for (int x = bx * PX_BLK; x < x1; ++x) {
+                const int j = map[y * o.w + x];
+                if (j < 0) continue;
+                const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                if (d2 < best || (d2 == best && j < bj)) {
+                  best = d2, bj = j;
+                  if (d2 < cut) cut = d2;
+                }
+              }
           }
-        }
       }
-      return;
-    }
+    if (best > gate2) bj = -1;
+    return;
   }
-  // generic clouds / degenerate projection: the reference's linear scan
+  // generic clouds: the reference's linear scan
   for (int j = 0; j < nt; ++j) {
     const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
     const double d2 = dx * dx + dy * dy + dz * dz;
@@ -599,7 +524,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs 
           const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
           double best;
           int bj;
-          nn_target(a.tgt, ti, toff, nt, a.cam, px, py, pz, it == 1 ? -1 : corr[i], cfg.gate2, best, bj);
+          nn_target(a.tgt, ti, toff, nt, px, py, pz, it == 1 ? -1 : corr[i], cfg.gate2, best, bj);
           int cj = -1;
           if (bj >= 0 && !(best > cfg.gate2)) {
             const double* cai = ca + 9 * (size_t)i;

@@ -75,21 +75,18 @@ struct CloudsDev {
   const int4* bbox;         // (n) screen box (gu_lo, gv_lo, gw, gh); null for uploaded clouds
 };
 
-// "Anything within the gate?" bits over a coarse 3-D grid covering one target's
-// AABB grown by pad >= gate (see px_gicp.cu).
-struct TgtNear {
-  double ox, oy, oz, inv_h;
-  int nx, ny, nz;
-  int rd;              // dilation radius in cells: floor(gate/h)+1
-  long long bit_off;   // into near_bits (32-bit words)
-};
-
 // Organised view of one target: its points are observed-cloud points, i.e. they
 // sit on stride-grid pixels of the frame.  map[(gy-gy0)*w + (gx-gx0)] = local
 // index or -1.  w == 0: not organised (generic cloud) -> linear scans.
+// boxes: 3-D bounding boxes {lo xyz, hi xyz} of the points of every PX_BLK x
+// PX_BLK block of map cells (bh x bw of them) followed by those of every PX_BLK x
+// PX_BLK group of blocks (sh x sw).
+#define PX_BLK 4
 struct TgtOrg {
   int gx0, gy0, w, h;
+  int bw, bh, sw, sh;
   long long map_off;
+  long long box_off;  // in boxes (units of 6 doubles)
 };
 
 struct TargetsDev {
@@ -97,21 +94,10 @@ struct TargetsDev {
   const long long* offset;  // (n_targets+1)
   const double* points;     // (sum,3)
   const double* cov;        // (sum,9)
-  const TgtNear* near;      // (n_targets)
-  const uint32_t* near_bits;
   const TgtOrg* org;        // (n_targets) or null
   const int32_t* tmap;
+  const double* boxes;
 };
-
-#define PX_GRID_MAX_CELLS 32768
-struct NearBuildArgs {
-  int n_targets;
-  const long long* offset;
-  const double* points;
-  const TgtNear* near;
-  uint32_t* near_bits;
-};
-cudaError_t launch_target_near(const NearBuildArgs& a, cudaStream_t st);
 
 struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   int n_clouds;
