@@ -46,6 +46,8 @@ WORKLOADS = {
     "c1": ("c1_box_3dof", lambda n: dict(dyaw=np.radians(22.5) / n)),
     "c2": ("c2_twocyl_color1", lambda n: dict(dt=0.04 / n)),
     "c3": ("c3_clutter_3dof", lambda n: dict(dt=0.025, dyaw=np.radians(22.5) / n, max_proposals=None)),
+    "c3q": ("c3_clutter_3dof", lambda n: dict(dt=0.025, dyaw=np.radians(22.5) / n, max_proposals=None,
+                                              workspace=(-0.125, 0.125, -0.125, 0.125))),
     "c3s": ("c3_clutter_3dof", lambda n: dict(dt=0.08, dyaw=np.radians(22.5) / n, max_proposals=None)),
     "c4": ("c4_mixed_6dof", lambda n: dict(viewpoints=642 * n, n_inplane=36, z_step=0.01, max_proposals=None)),
 }

@@ -289,7 +289,9 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
       const double d2 = dx * dx + dy * dy + dz * dz;
       if (d2 <= cut) best = d2, bj = prev, cut = d2;
     }
-    const int32_t* map = T.tmap + o.map_off;
+    const int32_t* lstart = T.leaf_start + o.box_off + ti;  // (bw*bh + 1) entries per target
+    const double* lp = T.leaf_pts + 3 * toff;              // points grouped by block
+    const int32_t* lidx = T.leaf_idx + toff;                // their local indices
     const double* bb = T.boxes + 6 * o.box_off;          // blocks, row-major (bh x bw)
     const double* sb = bb + 6 * (long long)o.bw * o.bh;  // super-blocks, row-major (sh x sw)
     for (int sy = 0; sy < o.sh; ++sy)
@@ -299,18 +301,18 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
         for (int by = sy * PX_BLK; by < by1; ++by)
           for (int bx = sx * PX_BLK; bx < bx1; ++bx) {
             if (box_dist2(bb + 6 * (by * o.bw + bx), qx, qy, qz) > cut) continue;
-            const int y1 = min(o.h, (by + 1) * PX_BLK), x1 = min(o.w, (bx + 1) * PX_BLK);
-            for (int y = by * PX_BLK; y < y1; ++y)
-              for (int x = bx * PX_BLK; x < x1; ++x) {
-                const int j = map[y * o.w + x];
-                if (j < 0) continue;
-                const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
-                const double d2 = dx * dx + dy * dy + dz * dz;
-                if (d2 < best || (d2 == best && j < bj)) {
-                  best = d2, bj = j;
-                  if (d2 < cut) cut = d2;
-                }
+            // the block's points are stored contiguously (leaf array): no map indirection
+            const int b = by * o.bw + bx;
+            const int k0 = lstart[b], k1 = lstart[b + 1];
+            for (int k = k0; k < k1; ++k) {
+              const double dx = lp[3 * k] - qx, dy = lp[3 * k + 1] - qy, dz = lp[3 * k + 2] - qz;
+              const double d2 = dx * dx + dy * dy + dz * dz;
+              const int j = lidx[k];
+              if (d2 < best || (d2 == best && j < bj)) {
+                best = d2, bj = j;
+                if (d2 < cut) cut = d2;
               }
+            }
           }
       }
     if (best > gate2) bj = -1;
@@ -459,7 +461,7 @@ __device__ double gicp_objective(const double* __restrict__ src, int n, const do
   return f;
 }
 
-__global__ void __launch_bounds__(PX_GICP_WARPS * 32, 2) gicp_kernel(RefineArgs a) {
+__global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(RefineArgs a) {
   extern __shared__ double sm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * PX_GICP_WARPS + wid;

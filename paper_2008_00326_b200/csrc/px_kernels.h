@@ -9,7 +9,12 @@
 #define PX_RENDER_THREADS 128
 #define PX_TRI_SMEM 64      // meshes up to this many triangles use the per-pixel path
 #define PX_TILE_PIX 4096    // stride-grid pixels per shared-memory z tile (atomic path)
-#define PX_GICP_WARPS 8     // candidates (warps) per CTA in the GICP kernel
+#ifndef PX_GICP_WARPS
+#define PX_GICP_WARPS 4     // candidates (warps) per CTA in the GICP kernel
+#endif
+#ifndef PX_GICP_MINB
+#define PX_GICP_MINB 4      // min resident CTAs per SM requested from ptxas (register budget: 128/thread)
+#endif
 #define PX_COST_WARPS 4
 #define PX_KCOV_MAX 32
 
@@ -97,6 +102,9 @@ struct TargetsDev {
   const TgtOrg* org;        // (n_targets) or null
   const int32_t* tmap;
   const double* boxes;
+  const int32_t* leaf_start;  // per target bw*bh+1 entries at [box_off + target index]
+  const double* leaf_pts;     // (sum,3) points grouped by block, same offsets as `points`
+  const int32_t* leaf_idx;    // (sum) local index of every grouped point
 };
 
 struct CovArgs {  // covariances of a list of clouds (targets), thread per point
