@@ -65,16 +65,7 @@ def build_workload(name: str, n_gpus: int):
     return frame, models, cfg, plan
 
 
-def shard_index(plan, rank: int, world: int) -> np.ndarray:
-    """Candidates of this rank: grid cells (3-DoF) / rotation blocks (6-DoF) dealt
-    round-robin so every target cloud stays on one rank and load is interleaved."""
-    if world == 1:
-        return np.arange(plan.n)
-    key = np.empty(plan.n, dtype=np.int64)
-    for oid in plan.active:
-        sel = np.nonzero(plan.flat_oid == oid)[0]
-        key[sel] = plan.proposal_sets[oid].provenance[plan.flat_local[sel], 0]
-    return np.nonzero(key % world == rank)[0]
+from paper_2008_00326_b200.dist import keys_from_device, shard_index  # noqa: E402
 
 
 class ClockSampler:
@@ -176,8 +167,7 @@ def run_gpu(args):
     def reduce_keys(out):
         """The only collective: min over ranks of (total << 32 | rank-in-object) per object."""
         if world > 1:
-            k = np.array([out.best_keys.get(oid, 2**63 - 1) & (2**63 - 1) for oid in plan.active], dtype=np.int64)
-            keys_t.copy_(torch.from_numpy(k))
+            keys_t.copy_(torch.from_numpy(keys_from_device(plan, out.best_keys)))
             dist.all_reduce(keys_t, op=dist.ReduceOp.MIN)
 
     # ---- resident-input arm (`value`) ----

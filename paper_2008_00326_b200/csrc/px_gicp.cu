@@ -16,6 +16,9 @@
 // BLAS fused orders (px_common.cuh); np.linalg.solve is LAPACK dgesv's
 // algorithm (partial-pivot LU); orthonormalize is the polar projection.
 // Compiled with -fmad=false.
+#include <cstdio>
+#include <cstring>
+
 #include "px_kernels.h"
 
 namespace px {
@@ -265,6 +268,13 @@ cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
 // member (floating-point subtraction, multiplication and addition are
 // monotone), so no candidate is ever skipped.
 
+#ifdef PX_NN_STATS
+__device__ unsigned long long g_nn_stats[8];  // queries, with-prev, sb tests, blk tests, leaf pts, found, leaves opened
+#define NN_STAT(i, v) atomicAdd(&g_nn_stats[i], (unsigned long long)(v))
+#else
+#define NN_STAT(i, v)
+#endif
+
 __device__ __forceinline__ double box_dist2(const double* __restrict__ b, double qx, double qy, double qz) {
   // b = {xlo, ylo, zlo, xhi, yhi, zhi}; empty boxes hold +inf / -inf and give +inf
   const double dx = fmax(fmax(b[0] - qx, qx - b[3]), 0.0);
@@ -284,7 +294,9 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
   const TgtOrg o = T.org ? T.org[ti] : TgtOrg{0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (o.w > 0) {
     double cut = gate2;
+    NN_STAT(0, 1);
     if (prev >= 0) {
+      NN_STAT(1, 1);
       const double dx = P[3 * prev] - qx, dy = P[3 * prev + 1] - qy, dz = P[3 * prev + 2] - qz;
       const double d2 = dx * dx + dy * dy + dz * dz;
       if (d2 <= cut) best = d2, bj = prev, cut = d2;
@@ -296,14 +308,18 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
     const double* sb = bb + 6 * (long long)o.bw * o.bh;  // super-blocks, row-major (sh x sw)
     for (int sy = 0; sy < o.sh; ++sy)
       for (int sx = 0; sx < o.sw; ++sx) {
+        NN_STAT(2, 1);
         if (box_dist2(sb + 6 * (sy * o.sw + sx), qx, qy, qz) > cut) continue;
         const int by1 = min(o.bh, (sy + 1) * PX_BLK), bx1 = min(o.bw, (sx + 1) * PX_BLK);
         for (int by = sy * PX_BLK; by < by1; ++by)
           for (int bx = sx * PX_BLK; bx < bx1; ++bx) {
+            NN_STAT(3, 1);
             if (box_dist2(bb + 6 * (by * o.bw + bx), qx, qy, qz) > cut) continue;
             // the block's points are stored contiguously (leaf array): no map indirection
             const int b = by * o.bw + bx;
             const int k0 = lstart[b], k1 = lstart[b + 1];
+            NN_STAT(4, k1 - k0);
+            NN_STAT(6, 1);
             for (int k = k0; k < k1; ++k) {
               const double dx = lp[3 * k] - qx, dy = lp[3 * k + 1] - qy, dz = lp[3 * k + 2] - qz;
               const double d2 = dx * dx + dy * dy + dz * dz;
@@ -316,6 +332,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
           }
       }
     if (best > gate2) bj = -1;
+    NN_STAT(5, bj >= 0);
     return;
   }
   // generic clouds: the reference's linear scan
@@ -730,6 +747,18 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(
   }
 }
 
+#ifdef PX_NN_STATS
+void dump_nn_stats() {
+  unsigned long long h[8];
+  cudaMemcpyFromSymbol(h, g_nn_stats, sizeof h);
+  if (h[0])
+    fprintf(stderr, "[nn stats] queries %llu, with prev %.3f, found %.3f; per query: sb tests %.2f, blk tests %.2f, leaves %.2f, leaf pts %.2f\n",
+            h[0], (double)h[1] / h[0], (double)h[5] / h[0], (double)h[2] / h[0], (double)h[3] / h[0], (double)h[6] / h[0], (double)h[4] / h[0]);
+  memset(h, 0, sizeof h);
+  cudaMemcpyToSymbol(g_nn_stats, h, sizeof h);
+}
+#endif
+
 cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st) {
   if (a.src.n == 0) return cudaSuccess;
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
@@ -737,6 +766,10 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
   gicp_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a);
+#ifdef PX_NN_STATS
+  cudaStreamSynchronize(st);
+  dump_nn_stats();
+#endif
   return cudaGetLastError();
 }
 

@@ -355,7 +355,7 @@ def _plan_targets(plan: SearchPlan, models, cam_to_world) -> None:
 
 @dataclass
 class StageOutputs:
-    """Per-candidate outputs of the device (or, in tests, oracle) stages."""
+    """Per-candidate outputs of the render / refine / cost stages."""
 
     refined_cam: np.ndarray   # (N,3,4)
     reg_T: np.ndarray         # (N,3,4) applied GICP correction (identity if none)

@@ -1,0 +1,153 @@
+"""CPU tests of the host-side mirror of the reference interface and of the C-ABI
+surface (no compute calls: those need a GPU)."""
+
+import ctypes
+import json
+import math
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import golden_io as G
+import paper_2008_00326_b200 as px
+from paper_2008_00326_b200 import _native
+from paper_2008_00326_b200.errors import ConfigError, DeviceError, EmptyBatch
+from paper_2008_00326_b200.proposals import _inclusive_range, compose_many
+from paper_2008_00326_b200.search import assemble_result, plan_search, StageOutputs
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_cabi_exports_every_declared_symbol():
+    """libpx.so loads without a GPU and exports exactly what include/px.h declares."""
+    header = (ROOT / "include" / "px.h").read_text()
+    declared = set(re.findall(r"\b(px_[a-z_0-9]+)\s*\(", header))
+    lib = ctypes.CDLL(str(_native.lib_path()))
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
+
+
+def test_no_cpu_fallback_without_device():
+    """Without a CUDA device the product fails loudly (never a silent CPU path)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(DeviceError, match="no CUDA device|CUDA"):
+        px.engine.Engine(0) if hasattr(px, "engine") else __import__("paper_2008_00326_b200.engine", fromlist=["Engine"]).Engine(0)
+    d, frame, models, cfg, plan = G.scene("c1_box_3dof")
+    with pytest.raises(DeviceError):
+        px.estimate_poses(frame, models, cfg)
+    with pytest.raises(DeviceError):
+        px.rendered_cost(plan.observed.subset(np.arange(5)), plan.observed, px.CostParams())
+
+
+def test_product_never_imports_oracle():
+    for f in (ROOT / "paper_2008_00326_b200").rglob("*.py"):
+        assert "oracle" not in f.read_text(), f
+    for f in (ROOT / "paper_2008_00326_b200" / "csrc").iterdir():
+        if f.is_file():
+            txt = f.read_text()
+            assert "px_oracle" not in txt and "liborc" not in txt, f
+
+
+def test_search_config_validation_and_roundtrip():
+    # reference search.py:63-81, 91-144
+    with pytest.raises(ConfigError):
+        px.SearchConfig(mode="9dof")
+    with pytest.raises(ConfigError):
+        px.SearchConfig(mode="3dof")  # workspace required
+    with pytest.raises(ConfigError):
+        px.SearchConfig(mode="3dof", workspace=(1, 0, 0, 1))
+    with pytest.raises(ConfigError):
+        px.SearchConfig(stride=0)
+    with pytest.raises(ConfigError):
+        px.SearchConfig(delta=0.0)
+    with pytest.raises(ConfigError):
+        px.SearchConfig.from_dict({"bogus": 1})
+    with pytest.raises(ConfigError):
+        px.SearchConfig.from_dict({"gicp": {"k_covariance": 2}})
+    c = px.SearchConfig(mode="3dof", workspace=(-0.4, 0.4, -0.4, 0.4), dyaw=math.radians(10.0), workers=3)
+    c2 = px.SearchConfig.from_dict(c.to_dict())
+    assert c2.workspace == c.workspace and abs(c2.dyaw - c.dyaw) < 1e-15 and c2.gicp == c.gicp
+    assert c.cost_params == px.CostParams(c.delta, c.tau_c, c.use_color) and c.knn_config.k == 1
+
+
+def test_select_best_and_types():
+    from paper_2008_00326_b200 import CostBreakdown
+    costs = [CostBreakdown(3, 4), CostBreakdown(1, 2), CostBreakdown(2, 1), CostBreakdown(9, 9)]
+    assert px.select_best(costs) == 1          # ties -> lowest index (search.py:178-183)
+    with pytest.raises(EmptyBatch):
+        px.select_best([])
+    with pytest.raises(ValueError):
+        CostBreakdown(-1, 0)
+    with pytest.raises(ValueError):
+        px.GicpConfig(k_covariance=3)
+    with pytest.raises(ValueError):
+        px.RigidTransform(np.eye(3) * 2.0, np.zeros(3))
+    cyl = px.InscribedCylinder(0.05, 0.0, 0.1)
+    assert cyl.contains(np.array([[0.05, 0.0, 0.05], [0.050001, 0.0, 0.05]])).tolist() == [True, False]
+
+
+def test_inclusive_range_reference_behaviour():
+    # proposals.py:97-105 always appends `hi` when the last step falls short
+    assert np.allclose(_inclusive_range(0.0, 0.05, 0.08), [0.0, 0.05])
+    assert len(_inclusive_range(-0.4, 0.4, 0.08)) == 11
+    g = px.grid_proposals_3dof((-0.4, 0.4, -0.4, 0.4), 0.08, math.radians(22.5), 0.0)
+    assert len(g) == 11 * 11 * 16 and g.provenance[-1].tolist() == [120, 15]
+    s = px.grid_proposals_3dof((-0.4, 0.4, -0.4, 0.4), 0.08, math.radians(22.5), 0.0, yaw_symmetric=True)
+    assert len(s) == 121
+
+
+def test_compose_many_matches_per_item_bits():
+    rng = np.random.default_rng(0)
+    from paper_2008_00326_b200.geometry import rotation_about_axis
+    a = px.RigidTransform(rotation_about_axis(rng.normal(size=3), 0.7), rng.normal(size=3))
+    rots = np.stack([rotation_about_axis(rng.normal(size=3), rng.uniform(-3, 3)) for _ in range(40)])
+    trs = rng.normal(size=(40, 3))
+    for t in (a, a.inverse()):  # C-contiguous rotation and transposed view
+        r, tr = compose_many(t, rots, trs)
+        for i in range(40):
+            ref = t.compose(px.RigidTransform(rots[i], trs[i]))
+            assert np.array_equal(r[i], ref.rotation) and np.array_equal(tr[i], ref.translation)
+
+
+def test_quantize_frame_is_disk_roundtrip_equivalent():
+    d, frame, models, cfg, plan = G.scene("c2_twocyl_color1")
+    q = px.quantize_frame(frame)  # fixture frames already went through the reference's save/load
+    assert np.array_equal(q.color, frame.color) and np.array_equal(q.depth.values, frame.depth.values)
+    assert np.array_equal(q.labels, frame.labels) and np.array_equal(q.depth.valid, frame.depth.valid)
+
+
+def test_assemble_result_and_json():
+    d, frame, models, cfg, plan = G.scene("c4_mixed_6dof")
+    out = StageOutputs(plan.cam_poses.copy(), np.tile(np.hstack([np.eye(3), np.zeros((3, 1))]), (plan.n, 1, 1)),
+                       d["j_o"].copy(), d["j_r"].copy(), n_rendered=d["n1"])
+    res = assemble_result(plan, out, 0.0)
+    js = json.loads(px.result_to_json(res))
+    ref = json.loads(str(d["result_json"]))
+    assert set(res.stage_millis) == {"render", "refine", "rerender", "cost"}
+    for a, b in zip(js["objects"], ref["objects"]):
+        assert (a["object_id"], a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == \
+               (b["object_id"], b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
+    assert "stage_millis" in json.loads(px.timings_to_json(res))
+
+
+def test_plan_failures_are_data():
+    # search.py:237-251: unknown objects are per-object failures, not exceptions
+    d, frame, models, cfg, plan = G.scene("c4_mixed_6dof")
+    fewer = {k: v for k, v in models.items() if k != 2}
+    p = plan_search(frame, fewer, cfg, build_targets=False)
+    assert p.failures == {2: "unknown_object"} and 2 not in p.active
+    out = StageOutputs(p.cam_poses, p.cam_poses, np.zeros(p.n, np.int32), np.zeros(p.n, np.int32))
+    est = assemble_result(p, out, 0.0).estimate_for(2)
+    assert est.failed and est.failure == "unknown_object"
+    with pytest.raises(ConfigError):
+        plan_search(dataclass_replace(frame, detections=[]), models, cfg)
+
+
+def dataclass_replace(obj, **kw):
+    import dataclasses
+    return dataclasses.replace(obj, **kw)
