@@ -49,11 +49,14 @@ WORKLOADS = {
     "c3q": ("c3_clutter_3dof", lambda n: dict(dt=0.025, dyaw=np.radians(22.5) / n, max_proposals=None,
                                               workspace=(-0.125, 0.125, -0.125, 0.125))),
     "c3s": ("c3_clutter_3dof", lambda n: dict(dt=0.08, dyaw=np.radians(22.5) / n, max_proposals=None)),
+    # C5 sweep: the C3 scene with the yaw axis refined `--scale` times (58,320 x scale candidates, same 3,645 targets)
+    "c5": ("c3_clutter_3dof", lambda n: dict(dt=0.025, dyaw=np.radians(22.5) / n, max_proposals=None)),
     "c4": ("c4_mixed_6dof", lambda n: dict(viewpoints=642 * n, n_inplane=36, z_step=0.01, max_proposals=None)),
 }
 
 
-def build_workload(name: str, n_gpus: int):
+def build_workload(name: str, n_gpus: int, scale: int = 1):
+    n_gpus = n_gpus * max(1, scale)
     import golden_io as G
     from paper_2008_00326_b200.search import plan_search
 
@@ -148,7 +151,7 @@ def run_gpu(args):
 
     from paper_2008_00326_b200.engine import Engine
 
-    frame, models, cfg, plan = build_workload(args.workload, world)
+    frame, models, cfg, plan = build_workload(args.workload, world, args.scale)
     idx = shard_index(plan, rank, world)
     eng = Engine(local)
     stream = torch.cuda.current_stream()
@@ -325,7 +328,7 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    frame, models, cfg, plan = build_workload(args.workload, world)
+    frame, models, cfg, plan = build_workload(args.workload, world, args.scale)
     from oracle import oracle as O
 
     cores = os.cpu_count() or 1
@@ -362,6 +365,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=3000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scale", type=int, default=1, help="refine the yaw/viewpoint axis: candidates x scale (C5 sweep)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     import __graft_entry__ as ge

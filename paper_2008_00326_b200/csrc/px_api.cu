@@ -95,6 +95,7 @@ struct px_ctx {
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
   double stage_ms[4] = {0, 0, 0, 0};
+  int chunks = 0;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -989,7 +990,8 @@ int px_search_upload(px_ctx* ctx, int64_t n, const int32_t* object_ids, const do
   return 0;
 }
 
-static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64_t hi, bool timed) {
+static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64_t hi) {
+  const bool timed = true;
   const int64_t n = hi - lo;
   if (n <= 0) return 0;
   const int32_t* slot = ctx->c_slot.as<int32_t>() + lo;
@@ -1001,8 +1003,8 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   const long long per_slot = 56 + (cfg->refine ? 148 : 0);
   if (total * per_slot > ctx->scratch_budget && n > 1024) {
     const int64_t mid = lo + n / 2;
-    if (int r = search_range(ctx, cfg, lo, mid, false)) return r;
-    return search_range(ctx, cfg, mid, hi, false);
+    if (int r = search_range(ctx, cfg, lo, mid)) return r;
+    return search_range(ctx, cfg, mid, hi);
   }
   if (int r = render_clouds(ctx, ctx->clouds, slot, pose_in, n, cfg->occluder_marking, cfg->delta)) return r;
   CU(cudaMemcpyAsync(ctx->r_cap0.as<long long>() + lo, ctx->clouds.cap.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1044,6 +1046,13 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
                        ctx->r_key.as<unsigned long long>()))
     return r;
   if (timed) CU(cudaEventRecord(ctx->ev[4], ctx->stream));
+  // per-chunk stage times accumulate (a split run is a sequence of such chunks)
+  CU(cudaEventSynchronize(ctx->ev[4]));
+  for (int i = 0; i < 4; ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) ctx->stage_ms[i] += ms;
+  }
+  ctx->chunks += 1;
   return 0;
 }
 
@@ -1079,15 +1088,9 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
   }
   for (double& m : ctx->stage_ms) m = 0.0;
   if (n == 0) return 0;
-  if (int r = search_range(ctx, cfg, 0, n, true)) return r;
+  ctx->chunks = 0;
+  if (int r = search_range(ctx, cfg, 0, n)) return r;
   CU(cudaStreamSynchronize(ctx->stream));
-  float ms;
-  // events are only recorded on the un-split path; a split run reports zeros
-  if (cudaEventQuery(ctx->ev[4]) == cudaSuccess) {
-    for (int i = 0; i < 4; ++i)
-      if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) ctx->stage_ms[i] = ms;
-  }
-  cudaGetLastError();
   return 0;
 }
 

@@ -12,10 +12,11 @@ import bench  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c3s")
 ap.add_argument("--steps", type=int, default=2)
+ap.add_argument("--scale", type=int, default=1)
 a = ap.parse_args()
 from paper_2008_00326_b200.engine import Engine  # noqa: E402
 
-frame, models, cfg, plan = bench.build_workload(a.workload, 1)
+frame, models, cfg, plan = bench.build_workload(a.workload, 1, a.scale)
 eng = Engine(0)
 eng.prepare_plan(frame, models, plan)
 n = eng.search_upload(plan)
@@ -23,4 +24,8 @@ sc = eng.search_cfg(plan)
 for _ in range(a.steps):
     eng.search_run(sc)
 out = eng.search_download(n)
-print("candidates", n, "stage_ms", out.stage_millis)
+import time
+t0 = time.perf_counter()
+eng.search_run(sc)
+eng.sync()
+print("candidates", n, "stage_ms", out.stage_millis, "wall_ms", (time.perf_counter() - t0) * 1e3)
