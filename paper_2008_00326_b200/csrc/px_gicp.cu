@@ -443,19 +443,19 @@ __device__ __forceinline__ void orthonormalize3(const double* r, double* x) {
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
-// fixed-association objective, registration.py:387-407; uniform result in all lanes
+// fixed-association objective, registration.py:387-407; uniform result in all lanes.
+// Per-point terms are written to `sbuf` (32 doubles of shared memory per warp) and
+// every lane adds them in source-index order (absent points add an exact +0).
 __device__ double gicp_objective(const double* __restrict__ src, int n, const double* __restrict__ tgt,
                                  const int32_t* __restrict__ corr, const double* __restrict__ wb,
-                                 const double* r, const double* t, int lane) {
+                                 const double* r, const double* t, int lane, double* sbuf) {
   double f = 0.0;
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
     double term = 0.0;
-    bool on = false;
     if (i < n) {
       const int j = corr[i];
       if (j >= 0) {
-        on = true;
         const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
         const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
         const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
@@ -468,12 +468,11 @@ __device__ double gicp_objective(const double* __restrict__ src, int n, const do
         term = dx * wd0 + dy * wd1 + dz * wd2;
       }
     }
-    unsigned vm = __ballot_sync(0xffffffffu, on);
-    while (vm) {
-      const int j = __ffs(vm) - 1;
-      vm &= vm - 1;
-      f += shfl_d(term, j);
-    }
+    sbuf[lane] = term;
+    __syncwarp();
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) f += sbuf[j];
+    __syncwarp();
   }
   return f;
 }
@@ -587,39 +586,59 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(
 #pragma unroll
               for (int q = 0; q < 9; ++q) wo[q] = w[q];
               const double dx = tgt[3 * bj] - px, dy = tgt[3 * bj + 1] - py, dz = tgt[3 * bj + 2] - pz;
-              const double J[3][6] = {{0.0, -pz, py, -1.0, 0.0, 0.0},
-                                      {pz, 0.0, -px, 0.0, -1.0, 0.0},
-                                      {-py, px, 0.0, 0.0, 0.0, -1.0}};
+              // J = [ [p]x | -I ] (registration.py:296-309).  The products with J's exact
+              // zeros and -1s are dropped / turned into negations below: x*0 = +-0 and
+              // a + (+-0) = a never change a non-zero value, (-1)*x = -x and a + (-b) = a - b
+              // are exact, and the sign of an all-zero term cannot survive the +0-initialised
+              // accumulators -- so every staged term has the reference's bits.
               const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
               const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
               const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
               stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
-#pragma unroll
-              for (int u = 0; u < 6; ++u)
-                stage[(36 + u) * STAGE_LD + lane] = -(J[0][u] * wd0 + J[1][u] * wd1 + J[2][u] * wd2);
+              // g[u] -= J[0][u]*wd0 + J[1][u]*wd1 + J[2][u]*wd2  (staged negated)
+              stage[36 * STAGE_LD + lane] = -(pz * wd1 - py * wd2);
+              stage[37 * STAGE_LD + lane] = -(px * wd2 - pz * wd0);
+              stage[38 * STAGE_LD + lane] = -(py * wd0 - px * wd1);
+              stage[39 * STAGE_LD + lane] = wd0;
+              stage[40 * STAGE_LD + lane] = wd1;
+              stage[41 * STAGE_LD + lane] = wd2;
+              // wj[q][u] = w[q][0]*J[0][u] + w[q][1]*J[1][u] + w[q][2]*J[2][u]
               double wj[3][6];
 #pragma unroll
-              for (int q = 0; q < 3; ++q)
+              for (int q = 0; q < 3; ++q) {
+                wj[q][0] = w[3 * q + 1] * pz - w[3 * q + 2] * py;
+                wj[q][1] = w[3 * q + 2] * px - w[3 * q] * pz;
+                wj[q][2] = w[3 * q] * py - w[3 * q + 1] * px;
+                wj[q][3] = -w[3 * q], wj[q][4] = -w[3 * q + 1], wj[q][5] = -w[3 * q + 2];
+              }
+              // h[u][v] += J[0][u]*wj[0][v] + J[1][u]*wj[1][v] + J[2][u]*wj[2][v]
 #pragma unroll
-                for (int u = 0; u < 6; ++u)
-                  wj[q][u] = w[3 * q] * J[0][u] + w[3 * q + 1] * J[1][u] + w[3 * q + 2] * J[2][u];
-#pragma unroll
-              for (int u = 0; u < 6; ++u)
-#pragma unroll
-                for (int v = 0; v < 6; ++v)
-                  stage[(6 * u + v) * STAGE_LD + lane] = J[0][u] * wj[0][v] + J[1][u] * wj[1][v] + J[2][u] * wj[2][v];
+              for (int v = 0; v < 6; ++v) {
+                stage[(0 + v) * STAGE_LD + lane] = pz * wj[1][v] - py * wj[2][v];
+                stage[(6 + v) * STAGE_LD + lane] = px * wj[2][v] - pz * wj[0][v];
+                stage[(12 + v) * STAGE_LD + lane] = py * wj[0][v] - px * wj[1][v];
+                stage[(18 + v) * STAGE_LD + lane] = -wj[0][v];
+                stage[(24 + v) * STAGE_LD + lane] = -wj[1][v];
+                stage[(30 + v) * STAGE_LD + lane] = -wj[2][v];
+              }
             }
           }
           corr[i] = cj;
         }
+        if (!on) {  // absent points contribute exact zeros (x + 0 = x; the accumulators are never -0)
+#pragma unroll
+          for (int e = 0; e < 43; ++e) stage[e * STAGE_LD + lane] = 0.0;
+        }
         __syncwarp();  // stage writes visible to the summing lanes
-        unsigned vm = __ballot_sync(0xffffffffu, on);
-        n_corr += __popc(vm);
-        while (vm) {
-          const int j = __ffs(vm) - 1;
-          vm &= vm - 1;
-          acc0 += stage[lane * STAGE_LD + j];
-          if (lane < 11) acc1 += stage[(lane + 32) * STAGE_LD + j];
+        n_corr += __popc(__ballot_sync(0xffffffffu, on));
+        {
+          const double* row0 = stage + lane * STAGE_LD;
+          const double* row1 = stage + (lane < 11 ? lane + 32 : lane) * STAGE_LD;
+#pragma unroll 8
+          for (int j = 0; j < 32; ++j) {
+            acc0 += row0[j];
+            acc1 += row1[j];  // lanes >= 11 accumulate a duplicate that is never read
+          }
         }
         __syncwarp();
       }
@@ -660,7 +679,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(
             r_try[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
           t_try[i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
         }
-        f_try = gicp_objective(src, n, tgt, corr, wb, r_try, t_try, lane);
+        f_try = gicp_objective(src, n, tgt, corr, wb, r_try, t_try, lane, stage);
         if (isfinite(f_try) && f_try <= f0) {
           accepted = true;
           break;
