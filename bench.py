@@ -255,10 +255,17 @@ def run_gpu(args):
     dom = max(st, key=st.get)
     dom_ms = st[dom]
     achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tj = ROOT / "profiles" / "traffic.json"
+    kname = {"refine": "gicp_kernel", "render": "render_kernel", "rerender": "render_kernel", "cost": "cost_kernel"}[dom]
+    if tj.exists() and args.scale == 1 and world == 1:
+        traffic = json.loads(tj.read_text()).get(args.workload, {}).get(kname, {}).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "kernel": {"refine": "gicp_kernel", "render": "render_kernel", "rerender": "render_kernel",
                                           "cost": "cost_kernel"}[dom],
                 "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
+                "frac": achieved / hbm_peak, "traffic": traffic,
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of this kernel on this "
+                                "workload (profiles/traffic.json); null when no capture matches",
                 "algorithmic_bytes_per_launch": ab[dom], "kernel_ms": dom_ms,
                 "whole_step_achieved": ab["total"] / (ms_per_step * 1e-3) / 1e9,
                 "whole_step_frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
@@ -267,7 +274,7 @@ def run_gpu(args):
     # ---- CPU baseline on a bounded sample of the same workload (rank 0, N=1 only) ----
     cpu = None
     if world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(frame, models, plan, idx, args.cpu_sample)
+        cpu = cpu_baseline(frame, models, plan, idx, args.cpu_sample or 40000)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -333,7 +340,7 @@ def run_reference(args):
 
     cores = os.cpu_count() or 1
     idx = np.arange(plan.n)
-    pick = sample_groups(plan, idx, args.cpu_sample)
+    pick = sample_groups(plan, idx, args.cpu_sample or 20000)
     for _ in range(args.warmup):
         O.run_plan(frame, models, plan, n_threads=cores, index=pick[:128])
     times = []
@@ -363,7 +370,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=3000)
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="candidates in the bounded CPU sample (default 40000 for cpu_baseline, 20000 per --impl reference step)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--scale", type=int, default=1, help="refine the yaw/viewpoint axis: candidates x scale (C5 sweep)")
     args = ap.parse_args()
