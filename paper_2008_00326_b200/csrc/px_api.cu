@@ -82,7 +82,7 @@ struct px_ctx {
   long long tgt_total = 0;
   int tgt_k = 0;
   double tgt_gate = 0.0;
-  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts, tgt_lidx;
+  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
   bool tgt_organised = false;
   // resident candidates
   int64_t n_cand = 0;
@@ -326,7 +326,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
-                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->tgt_lidx, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
+                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
@@ -665,10 +665,9 @@ static TargetsDev targets_dev(px_ctx* ctx) {
   t.cov = ctx->tgt_cov.as<double>();
   t.org = ctx->tgt_organised ? ctx->tgt_org.as<TgtOrg>() : nullptr;
   t.tmap = ctx->tgt_map.as<int32_t>();
-  t.boxes = ctx->tgt_boxes.as<double>();
+  t.boxes32 = ctx->tgt_boxes.as<float>();
   t.leaf_start = ctx->tgt_lstart.as<int32_t>();
-  t.leaf_pts = ctx->tgt_lpts.as<double>();
-  t.leaf_idx = ctx->tgt_lidx.as<int32_t>();
+  t.leaf32 = ctx->tgt_lpts.as<float4>();
   return t;
 }
 
@@ -696,8 +695,9 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   bool org = obs_index != nullptr && ctx->have_scene && ctx->organised && !ctx->h_obs_src.empty();
   std::vector<TgtOrg> orgs((size_t)n_targets);
   std::vector<int32_t> tmap, tpix;
-  std::vector<double> boxes, lpts;
-  std::vector<int32_t> lstart, lidx;
+  std::vector<double> boxes;   // {lo xyz, hi xyz} per node, converted to fp32 centre/half-extent below
+  std::vector<float> boxes32, leaf32;
+  std::vector<int32_t> lstart;
   if (org) {
     const int st = ctx->cam.stride;
     tpix.resize((size_t)total);
@@ -753,8 +753,7 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
       }
       // leaf arrays: every target's points grouped by block (ascending local index inside a block)
       lstart.assign((size_t)(box_total + n_targets), 0);
-      lpts.resize((size_t)total * 3);
-      lidx.resize((size_t)total);
+      leaf32.resize((size_t)total * 4);
       for (int t = 0; t < n_targets; ++t) {
         const TgtOrg& o = orgs[(size_t)t];
         const long long a = off[(size_t)t], b = off[(size_t)t + 1];
@@ -770,10 +769,36 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
         for (int q = 0; q <= nb_; ++q) ls[q] = cnt[(size_t)q];
         for (long long i = a; i < b; ++i) {
           const int k = cnt[(size_t)blk(i)]++;
-          for (int d = 0; d < 3; ++d) lpts[(size_t)(3 * (a + k) + d)] = points[3 * i + d];
-          lidx[(size_t)(a + k)] = (int32_t)(i - a);
+          for (int d = 0; d < 3; ++d) leaf32[(size_t)(4 * (a + k) + d)] = (float)points[3 * i + d];
+          const int32_t li = (int32_t)(i - a);
+          memcpy(&leaf32[(size_t)(4 * (a + k) + 3)], &li, 4);
         }
       }
+    }
+  }
+  if (org) {
+    // fp32 pruning copies: centre / half-extent with the half-extent inflated by the centre's
+    // rounding (rounded up), and the per-target bound `err` on all fp32 rounding in the tests
+    boxes32.resize(boxes.size());
+    for (size_t q = 0; q < boxes.size() / 6; ++q) {
+      for (int d = 0; d < 3; ++d) {
+        const double lo = boxes[6 * q + d], hi = boxes[6 * q + 3 + d];
+        float cf = 0.f, hf = -1e30f;  // empty node: distance overflows to +inf and is always pruned
+        if (lo <= hi) {
+          const double c = 0.5 * (lo + hi);
+          cf = (float)c;
+          const double h = std::max(hi - (double)cf, (double)cf - lo);
+          hf = (float)h;
+          if ((double)hf < h) hf = std::nextafterf(hf, INFINITY);
+        }
+        boxes32[6 * q + d] = cf, boxes32[6 * q + 3 + d] = hf;
+      }
+    }
+    for (int t = 0; t < n_targets; ++t) {
+      double m = 0.0;
+      for (long long i = off[(size_t)t]; i < off[(size_t)t + 1]; ++i)
+        for (int d = 0; d < 3; ++d) m = std::max(m, std::fabs(points[3 * i + d]));
+      orgs[(size_t)t].err = std::ldexp(1.5 * (2.0 * m + 1.0), -24);
     }
   }
   ctx->tgt_organised = org;
@@ -784,10 +809,9 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     if (int r = h2d(ctx, ctx->tgt_org, orgs.data(), orgs.size() * sizeof(TgtOrg))) return r;
     if (int r = h2d(ctx, ctx->tgt_map, tmap.data(), tmap.size() * 4)) return r;
     if (int r = h2d(ctx, ctx->tgt_pix, tpix.data(), tpix.size() * 4)) return r;
-    if (int r = h2d(ctx, ctx->tgt_boxes, boxes.data(), boxes.size() * 8)) return r;
+    if (int r = h2d(ctx, ctx->tgt_boxes, boxes32.data(), boxes32.size() * 4)) return r;
     if (int r = h2d(ctx, ctx->tgt_lstart, lstart.data(), lstart.size() * 4)) return r;
-    if (int r = h2d(ctx, ctx->tgt_lpts, lpts.data(), lpts.size() * 8)) return r;
-    if (int r = h2d(ctx, ctx->tgt_lidx, lidx.data(), lidx.size() * 4)) return r;
+    if (int r = h2d(ctx, ctx->tgt_lpts, leaf32.data(), leaf32.size() * 4)) return r;
   }
   const size_t tot1 = (size_t)std::max<long long>(total, 1);
   CU(ctx->tgt_cov.ensure(tot1 * 72));

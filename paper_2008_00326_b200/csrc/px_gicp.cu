@@ -283,59 +283,106 @@ __device__ __forceinline__ double box_dist2(const double* __restrict__ b, double
   return dx * dx + dy * dy + dz * dz;
 }
 
+// fp32 squared distance from a point to a box stored as centre / half-extent; the
+// half-extents were inflated on the host so that this never exceeds the exact
+// squared distance to any member point by more than the threshold slack.
+__device__ __forceinline__ float box_dist2f(const float* __restrict__ b, float qx, float qy, float qz) {
+  const float2 b0 = __ldg(reinterpret_cast<const float2*>(b)), b1 = __ldg(reinterpret_cast<const float2*>(b) + 1),
+               b2 = __ldg(reinterpret_cast<const float2*>(b) + 2);
+  const float gx = fmaxf(fabsf(qx - b0.x) - b1.y, 0.f);
+  const float gy = fmaxf(fabsf(qy - b0.y) - b2.x, 0.f);
+  const float gz = fmaxf(fabsf(qz - b1.x) - b2.y, 0.f);
+  return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+}
+
 // Lexicographic minimum of (d2, index) over the target points with d2 <= gate2,
 // identical to the reference's brute-force scan (registration.py:251-260)
 // whenever that scan's winner passes the gate; bj = -1 if no point is within the
 // gate.  `prev` (last iteration's correspondence, or -1) seeds the cut-off.
+//
+// Pruning runs in fp32 on conservatively rounded copies (boxes as centre /
+// half-extent, points as float3 + index): with e = T.org.err bounding every
+// rounding involved, a node or point whose fp32 squared distance exceeds
+//     thr = roundup_f32((sqrt(best) + 2e)^2 * (1 + 2^-20))
+// is provably farther than `best` in exact arithmetic, so it can neither beat nor
+// tie the current winner; everything else is evaluated in fp64 with the
+// reference's operation order on the original coordinates.  Results are therefore
+// bit-identical to the linear scan (tests: organised == generic).
+__device__ __forceinline__ float nn_threshold(double best, double err) {
+  const double s = sqrt(best) + 2.0 * err;
+  return __double2float_ru(s * s * (1.0 + 9.5367431640625e-07));
+}
+
 __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long toff, int nt, double qx, double qy,
                                           double qz, int prev, double gate2, double& best, int& bj) {
-  best = CUDART_INF, bj = -1;
   const double* P = T.points + 3 * toff;
-  const TgtOrg o = T.org ? T.org[ti] : TgtOrg{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const TgtOrg o = T.org ? T.org[ti] : TgtOrg{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0.0};
   if (o.w > 0) {
-    double cut = gate2;
+    // search state: (best, bj) = lexicographically smallest (d2, index) seen with d2 <= gate2
+    best = gate2, bj = 0x7fffffff;
     NN_STAT(0, 1);
     if (prev >= 0) {
       NN_STAT(1, 1);
       const double dx = P[3 * prev] - qx, dy = P[3 * prev + 1] - qy, dz = P[3 * prev + 2] - qz;
       const double d2 = dx * dx + dy * dy + dz * dz;
-      if (d2 <= cut) best = d2, bj = prev, cut = d2;
+      if (d2 <= best) best = d2, bj = prev;
     }
+    float thr = nn_threshold(best, o.err);
+    const float qxf = (float)qx, qyf = (float)qy, qzf = (float)qz;
     const int32_t* lstart = T.leaf_start + o.box_off + ti;  // (bw*bh + 1) entries per target
-    const double* lp = T.leaf_pts + 3 * toff;              // points grouped by block
-    const int32_t* lidx = T.leaf_idx + toff;                // their local indices
-    const double* bb = T.boxes + 6 * o.box_off;          // blocks, row-major (bh x bw)
-    const double* sb = bb + 6 * (long long)o.bw * o.bh;  // super-blocks, row-major (sh x sw)
+    const float4* lp = T.leaf32 + toff;                     // points grouped by block: {x, y, z, index bits}
+    const float* bb = T.boxes32 + 6 * o.box_off;            // blocks {cx,cy,cz,hx,hy,hz}, row-major (bh x bw)
+    const float* sb = bb + 6 * (long long)o.bw * o.bh;      // super-blocks, row-major (sh x sw)
     for (int sy = 0; sy < o.sh; ++sy)
       for (int sx = 0; sx < o.sw; ++sx) {
         NN_STAT(2, 1);
-        if (box_dist2(sb + 6 * (sy * o.sw + sx), qx, qy, qz) > cut) continue;
-        const int by1 = min(o.bh, (sy + 1) * PX_BLK), bx1 = min(o.bw, (sx + 1) * PX_BLK);
-        for (int by = sy * PX_BLK; by < by1; ++by)
-          for (int bx = sx * PX_BLK; bx < bx1; ++bx) {
-            NN_STAT(3, 1);
-            if (box_dist2(bb + 6 * (by * o.bw + bx), qx, qy, qz) > cut) continue;
-            // the block's points are stored contiguously (leaf array): no map indirection
-            const int b = by * o.bw + bx;
-            const int k0 = lstart[b], k1 = lstart[b + 1];
-            NN_STAT(4, k1 - k0);
-            NN_STAT(6, 1);
-            for (int k = k0; k < k1; ++k) {
-              const double dx = lp[3 * k] - qx, dy = lp[3 * k + 1] - qy, dz = lp[3 * k + 2] - qz;
-              const double d2 = dx * dx + dy * dy + dz * dz;
-              const int j = lidx[k];
-              if (d2 < best || (d2 == best && j < bj)) {
-                best = d2, bj = j;
-                if (d2 < cut) cut = d2;
-              }
-            }
+        if (box_dist2f(sb + 6 * (sy * o.sw + sx), qxf, qyf, qzf) > thr) continue;
+        // phase 1: test the (up to) 16 blocks of this super-block back to back -- independent loads and
+        // arithmetic, no control flow -- and collect the survivors in a bit mask
+        const int bx0 = sx * PX_BLK, by0 = sy * PX_BLK;
+        unsigned bmask = 0;
+#pragma unroll
+        for (int q = 0; q < PX_BLK * PX_BLK; ++q) {
+          const int by = by0 + (q >> 2), bx = bx0 + (q & 3);
+          const bool in = by < o.bh && bx < o.bw;
+          const float d = box_dist2f(bb + 6 * (in ? by * o.bw + bx : 0), qxf, qyf, qzf);
+          bmask |= (unsigned)(in && !(d > thr)) << q;
+        }
+        NN_STAT(3, PX_BLK * PX_BLK);
+        while (bmask) {
+          const int q = __ffs(bmask) - 1;
+          bmask &= bmask - 1;
+          const int b = (by0 + (q >> 2)) * o.bw + bx0 + (q & 3);
+          const int k0 = lstart[b], k1 = lstart[b + 1];
+          NN_STAT(4, k1 - k0);
+          NN_STAT(6, 1);
+          // phase 1 over the leaf (<= 16 points): fp32 squared distances, survivors into a mask
+          unsigned pmask = 0;
+#pragma unroll 4
+          for (int k = k0; k < k1; ++k) {
+            const float4 pf = __ldg(lp + k);
+            const float tx = pf.x - qxf, ty = pf.y - qyf, tz = pf.z - qzf;
+            pmask |= (unsigned)!(fmaf(tz, tz, fmaf(ty, ty, tx * tx)) > thr) << (k - k0);
           }
+          // phase 2: exact fp64 evaluation of the few survivors, reference operation order
+          bool improved = false;
+          while (pmask) {
+            const int k = k0 + __ffs(pmask) - 1;
+            pmask &= pmask - 1;
+            const int j = __float_as_int(__ldg(&lp[k].w));
+            const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;
+          }
+          if (improved) thr = nn_threshold(best, o.err);
+        }
       }
-    if (best > gate2) bj = -1;
+    if (bj == 0x7fffffff) best = CUDART_INF, bj = -1;
     NN_STAT(5, bj >= 0);
     return;
   }
   // generic clouds: the reference's linear scan
+  best = CUDART_INF, bj = -1;
   for (int j = 0; j < nt; ++j) {
     const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
     const double d2 = dx * dx + dy * dy + dz * dz;

@@ -91,7 +91,8 @@ struct TgtOrg {
   int gx0, gy0, w, h;
   int bw, bh, sw, sh;
   long long map_off;
-  long long box_off;  // in boxes (units of 6 doubles)
+  long long box_off;  // in boxes32 (units of 6 floats) / leaf_start
+  double err;         // bound on every fp32 rounding error of the pruning tests for this target (metres)
 };
 
 struct TargetsDev {
@@ -101,10 +102,9 @@ struct TargetsDev {
   const double* cov;        // (sum,9)
   const TgtOrg* org;        // (n_targets) or null
   const int32_t* tmap;
-  const double* boxes;
+  const float* boxes32;       // per node {cx,cy,cz,hx,hy,hz}: fp32 centre / inflated half-extent of the 3-D box
   const int32_t* leaf_start;  // per target bw*bh+1 entries at [box_off + target index]
-  const double* leaf_pts;     // (sum,3) points grouped by block, same offsets as `points`
-  const int32_t* leaf_idx;    // (sum) local index of every grouped point
+  const float4* leaf32;       // (sum) points grouped by block: fp32 copy {x,y,z} + local index bits
 };
 
 struct CovArgs {  // covariances of a list of clouds (targets), thread per point
