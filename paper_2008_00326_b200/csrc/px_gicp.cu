@@ -127,6 +127,9 @@ struct OrgView {
 // k nearest (d2, index)-lexicographic neighbours of point i sitting at map cell
 // (cx, cy); identical to the reference's brute-force insertion scan
 // (registration.py:117-142).  nd/ni come back sorted ascending.
+// S = element stride of the nd / ni lists (1: thread-local arrays; 32: one column per lane of a
+// warp-shared staging area, which keeps the lists out of the small L1).
+template <int S>
 __device__ __forceinline__ void knn_ring(const OrgView& V, int i, int cx, int cy, int k, double ray_k, double* nd, int* ni) {
   const double xi = V.pts[3 * i], yi = V.pts[3 * i + 1], zi = V.pts[3 * i + 2];
   int cnt = 0;
@@ -151,9 +154,10 @@ __device__ __forceinline__ void knn_ring(const OrgView& V, int i, int cx, int cy
           pos = k - 1;
         else
           continue;
-        while (pos > 0 && (nd[pos - 1] > d2 || (nd[pos - 1] == d2 && ni[pos - 1] > j))) nd[pos] = nd[pos - 1], ni[pos] = ni[pos - 1], --pos;
-        nd[pos] = d2, ni[pos] = j;
-        if (cnt == k) worst = nd[k - 1], worst_j = ni[k - 1];
+        while (pos > 0 && (nd[(pos - 1) * S] > d2 || (nd[(pos - 1) * S] == d2 && ni[(pos - 1) * S] > j)))
+          nd[pos * S] = nd[(pos - 1) * S], ni[pos * S] = ni[(pos - 1) * S], --pos;
+        nd[pos * S] = d2, ni[pos * S] = j;
+        if (cnt == k) worst = nd[(k - 1) * S], worst_j = ni[(k - 1) * S];
       }
     }
     if (cnt == k) {
@@ -165,15 +169,16 @@ __device__ __forceinline__ void knn_ring(const OrgView& V, int i, int cx, int cy
 
 // mean / covariance / Jacobi / regularised output for a sorted neighbour list
 // (registration.py:143-216)
+template <int S>
 __device__ __forceinline__ void cov_from_neighbours(const double* __restrict__ pts, const int* ni, int k, double eps,
                                                     double* __restrict__ out) {
   double mx = 0.0, my = 0.0, mz = 0.0;
-  for (int q = 0; q < k; ++q) mx += pts[3 * ni[q]], my += pts[3 * ni[q] + 1], mz += pts[3 * ni[q] + 2];
+  for (int q = 0; q < k; ++q) mx += pts[3 * ni[q * S]], my += pts[3 * ni[q * S] + 1], mz += pts[3 * ni[q * S] + 2];
   const double kd = (double)k;
   mx /= kd, my /= kd, mz /= kd;
   double a00 = 0, a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0;
   for (int q = 0; q < k; ++q) {
-    const double dx = pts[3 * ni[q]] - mx, dy = pts[3 * ni[q] + 1] - my, dz = pts[3 * ni[q] + 2] - mz;
+    const double dx = pts[3 * ni[q * S]] - mx, dy = pts[3 * ni[q * S] + 1] - my, dz = pts[3 * ni[q * S] + 2] - mz;
     a00 += dx * dx, a01 += dx * dy, a02 += dx * dz, a11 += dy * dy, a12 += dy * dz, a22 += dz * dz;
   }
   double a[3][3], vm[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
@@ -229,8 +234,14 @@ __device__ __forceinline__ void cov_from_neighbours(const double* __restrict__ p
 __device__ void cov_point_org(const OrgView& V, int i, int cx, int cy, int k, double eps, double ray_k, double* __restrict__ out) {
   double nd[PX_KCOV_MAX];
   int ni[PX_KCOV_MAX];
-  knn_ring(V, i, cx, cy, k, ray_k, nd, ni);
-  cov_from_neighbours(V.pts, ni, k, eps, out);
+  knn_ring<1>(V, i, cx, cy, k, ray_k, nd, ni);
+  cov_from_neighbours<1>(V.pts, ni, k, eps, out);
+}
+// same, with the neighbour lists in a warp-shared area (column `lane`, stride 32)
+__device__ void cov_point_org_sm(const OrgView& V, int i, int cx, int cy, int k, double eps, double ray_k,
+                                 double* __restrict__ out, double* nd, int* ni) {
+  knn_ring<32>(V, i, cx, cy, k, ray_k, nd, ni);
+  cov_from_neighbours<32>(V.pts, ni, k, eps, out);
 }
 
 // one CTA per target cloud, threads over its points
@@ -567,8 +578,17 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(
       OrgView V{src, a.src.slot_map + off, bb.z, bb.w};
       const int32_t* spx = a.src.src_px + 2 * off;
       const int st = a.cam.stride;
-      for (int i = lane; i < n; i += 32)
-        cov_point_org(V, i, spx[2 * i] / st - bb.x, spx[2 * i + 1] / st - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k, ca + 9 * (size_t)i);
+      if (cfg.k_cov * 32 * 12 <= 43 * STAGE_LD * 8) {
+        // neighbour lists live in this warp's (still unused) staging area: [k][32] doubles + [k][32] ints
+        double* nd = stage + lane;
+        int* ni = reinterpret_cast<int*>(stage + cfg.k_cov * 32) + lane;
+        for (int i = lane; i < n; i += 32)
+          cov_point_org_sm(V, i, spx[2 * i] / st - bb.x, spx[2 * i + 1] / st - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k,
+                           ca + 9 * (size_t)i, nd, ni);
+      } else {
+        for (int i = lane; i < n; i += 32)
+          cov_point_org(V, i, spx[2 * i] / st - bb.x, spx[2 * i + 1] / st - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k, ca + 9 * (size_t)i);
+      }
     } else {
       for (int i = lane; i < n; i += 32) cov_point(src, n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
     }
