@@ -90,7 +90,7 @@ struct px_ctx {
   DevBuf c_slot, c_pose, c_tidx, c_rank;
   // search scratch / results
   CloudStore clouds;
-  DevBuf src_cov, w_buf, corr, total_dev;
+  DevBuf src_cov, w_buf, corr, nn, st_pose, st_i, total_dev;
   DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1;
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
@@ -277,8 +277,11 @@ int check_gicp(px_ctx* ctx, const px_gicp_cfg& g) {
   return 0;
 }
 
-int ensure_refine_scratch(px_ctx* ctx, long long total_cap) {
+int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   size_t tot = (size_t)std::max<long long>(total_cap, 1);
+  CU(ctx->nn.ensure(sizeof(int32_t) * tot));
+  CU(ctx->st_pose.ensure(sizeof(double) * 12 * (size_t)std::max<int64_t>(n_cand, 1)));
+  CU(ctx->st_i.ensure(sizeof(int32_t) * 8 * (size_t)std::max<int64_t>(n_cand, 1)));
   CU(ctx->src_cov.ensure(sizeof(double) * 9 * tot));
   CU(ctx->w_buf.ensure(sizeof(double) * 9 * tot));
   CU(ctx->corr.ensure(sizeof(int32_t) * tot));
@@ -327,7 +330,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
                     &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
-                    &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->total_dev, &ctx->r_T,
+                    &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
   for (DevBuf* b : bufs) b->release();
@@ -847,7 +850,7 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
     if (target_idx[i] < 0 || target_idx[i] >= ctx->n_targets) return fail(ctx, PX_E_ARG, "target index out of range");
   if (n == 0) return 0;
   CU(cudaSetDevice(ctx->device));
-  if (int r = ensure_refine_scratch(ctx, sources->s.total_cap)) return r;
+  if (int r = ensure_refine_scratch(ctx, sources->s.total_cap, n)) return r;
   DevBuf dti, dinit, dT, dit, dfl, dres, dtr, dnt;
   int rc = 0;
   do {
@@ -868,15 +871,17 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
     a.cfg = gicp_dev(*cfg);
     a.cam = ctx->cam;
     a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
     a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
     a.out_resid = out_residual ? dres.as<double>() : nullptr;
     a.out_trace = out_trace ? dtr.as<double>() : nullptr;
     a.out_ntrace = dnt.as<int32_t>();
-    if ((e = launch_refine(a, ctx->stream))) {
+    int nl = 0;
+    if ((e = launch_refine(a, ctx->stream, &nl))) {
       rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
       break;
     }
-    ctx->launches += 1;
+    ctx->launches += nl;
     if ((rc = d2h(ctx, out_T, dT.p, (size_t)n * 96)) || (rc = d2h(ctx, out_iters, dit.p, (size_t)n * 4)) ||
         (rc = d2h(ctx, out_flags, dfl.p, (size_t)n * 4)) || (rc = d2h(ctx, out_ntrace, dnt.p, (size_t)n * 4)) ||
         (out_residual && (rc = d2h(ctx, out_residual, dres.p, (size_t)n * 8))) ||
@@ -1024,7 +1029,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   long long total = 0;
   if (timed) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (int r = size_clouds(ctx, ctx->clouds, slot, pose_in, n, &total)) return r;
-  const long long per_slot = 56 + (cfg->refine ? 148 : 0);
+  const long long per_slot = 60 + (cfg->refine ? 152 : 0);
   if (total * per_slot > ctx->scratch_budget && n > 1024) {
     const int64_t mid = lo + n / 2;
     if (int r = search_range(ctx, cfg, lo, mid)) return r;
@@ -1036,7 +1041,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   if (timed) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
   const double* cost_pose = pose_in;
   if (cfg->refine) {
-    if (int r = ensure_refine_scratch(ctx, total)) return r;
+    if (int r = ensure_refine_scratch(ctx, total, n)) return r;
     RefineArgs a{};
     a.src = clouds_dev(ctx->clouds);
     a.tgt = targets_dev(ctx);
@@ -1044,6 +1049,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     a.cfg = gicp_dev(cfg->gicp);
     a.cam = ctx->cam;
     a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
     a.out_T = ctx->r_T.as<double>() + 12 * lo;
     a.out_iters = ctx->r_iters.as<int32_t>() + lo, a.out_flags = ctx->r_flags.as<int32_t>() + lo;
     a.out_ncorr_sum = ctx->r_ncorr.as<int32_t>() + lo;
@@ -1052,8 +1058,9 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     memcpy(a.c2w, cfg->cam_to_world, sizeof a.c2w);
     memcpy(a.w2c, cfg->world_to_cam, sizeof a.w2c);
     a.c2w_vec_order = cfg->c2w_vec_order, a.w2c_vec_order = cfg->w2c_vec_order, a.fixed_z = cfg->fixed_z;
-    CU(launch_refine(a, ctx->stream));
-    ctx->launches += 1;
+    int nl = 0;
+    CU(launch_refine(a, ctx->stream, &nl));
+    ctx->launches += nl;
     if (timed) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     if (int r = size_clouds(ctx, ctx->clouds, slot, pose_ref, n, &total)) return r;
     if (int r = render_clouds(ctx, ctx->clouds, slot, pose_ref, n, cfg->occluder_marking, cfg->delta)) return r;

@@ -16,6 +16,7 @@
 // BLAS fused orders (px_common.cuh); np.linalg.solve is LAPACK dgesv's
 // algorithm (partial-pivot LU); orthonormalize is the polar projection.
 // Compiled with -fmad=false.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -535,241 +536,330 @@ __device__ double gicp_objective(const double* __restrict__ src, int n, const do
   return f;
 }
 
-__global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(RefineArgs a) {
+// ---------------------------------------------------------------------------
+// The batched refinement runs iteration-synchronously over all candidates:
+//
+//   gicp_init_kernel   once   per-candidate state, source covariances
+//   gicp_nn_kernel     / it   exact nearest neighbours of every source point (no shared
+//                             memory, 64 registers: the whole 228 KB is L1 for the target
+//                             data and twice as many warps hide the dependent loads)
+//   gicp_step_kernel   / it   linearise with those neighbours, ordered sums, solve, step
+//                             halving, state update (128 registers, staging shared memory)
+//   gicp_finish_kernel once   result transform, residual, refine-apply + 3-DoF re-lift
+//
+// One warp per candidate in every kernel; a candidate that has finished (converged,
+// failed, stagnated) makes its warp exit immediately.  The arithmetic and its order are
+// exactly those of the reference loop (registration.py:410-476) -- only the place
+// where the loop counter lives changed.
+
+// per-candidate integer state (RefineArgs::st_i, 8 ints each)
+enum { ST_FAIL = 0, ST_DONE = 1, ST_ITERS = 2, ST_CONV = 3, ST_NTRACE = 4, ST_NCORR = 5 };
+
+struct CandView {
+  int n, nt, ti;
+  long long off, toff;
+};
+__device__ __forceinline__ CandView cand_view(const RefineArgs& a, int c) {
+  CandView v;
+  v.n = a.src.count[c];
+  v.off = a.src.offset[c];
+  v.ti = a.target_idx[c];
+  v.toff = a.tgt.offset[v.ti];
+  v.nt = (int)(a.tgt.offset[v.ti + 1] - v.toff);
+  return v;
+}
+
+__global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
+  extern __shared__ double sm[];  // per warp: [k][32] doubles + [k][32] ints of neighbour lists
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + wid;
+  if (c >= a.src.n) return;
+  const CandView v = cand_view(a, c);
+  const GicpCfgDev cfg = a.cfg;
+  const double* src = a.src.points + 3 * v.off;
+  double* ca = a.src_cov + 9 * v.off;
+  int* st = a.st_i + 8 * (size_t)c;
+  double* pose = a.st_pose + 12 * (size_t)c;
+  if (lane < 12) {
+    double val = (lane == 0 || lane == 4 || lane == 8) ? 1.0 : 0.0;  // [R | t] as 9 + 3
+    if (a.init_T) {
+      const double* T0 = a.init_T + 12 * (size_t)c;
+      val = lane < 9 ? T0[4 * (lane / 3) + lane % 3] : T0[4 * (lane - 9) + 3];
+    }
+    pose[lane] = val;
+  }
+  const bool too_few = v.n <= cfg.k_cov || v.nt <= cfg.k_cov;  // registration.py:504-510
+  if (lane < 8) st[lane] = lane == ST_FAIL ? (too_few ? F_TOO_FEW : F_OK) : (lane == ST_DONE ? (too_few || cfg.max_iter < 1) : 0);
+  if (too_few) return;
+  if (a.src.slot_map) {
+    const int4 bb = a.src.bbox[c];
+    OrgView V{src, a.src.slot_map + v.off, bb.z, bb.w};
+    const int32_t* spx = a.src.src_px + 2 * v.off;
+    const int stp = a.cam.stride;
+    double* nd = sm + (size_t)wid * (cfg.k_cov * 48) + lane;
+    int* ni = reinterpret_cast<int*>(sm + (size_t)wid * (cfg.k_cov * 48) + cfg.k_cov * 32) + lane;
+    for (int i = lane; i < v.n; i += 32)
+      cov_point_org_sm(V, i, spx[2 * i] / stp - bb.x, spx[2 * i + 1] / stp - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k,
+                       ca + 9 * (size_t)i, nd, ni);
+  } else {
+    for (int i = lane; i < v.n; i += 32) cov_point(src, v.n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
+  }
+}
+
+__global__ void __launch_bounds__(128, 8) gicp_nn_kernel(RefineArgs a, int it) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + wid;
+  if (c >= a.src.n) return;
+  if (a.st_i[8 * (size_t)c + ST_DONE]) return;
+  const CandView v = cand_view(a, c);
+  const double* src = a.src.points + 3 * v.off;
+  const int32_t* corr = a.corr + v.off;
+  int32_t* nn = a.nn + v.off;
+  double r[9], t[3];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) r[q] = a.st_pose[12 * (size_t)c + q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) t[q] = a.st_pose[12 * (size_t)c + 9 + q];
+  const double gate2 = a.cfg.gate2;
+  for (int i = lane; i < v.n; i += 32) {
+    const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
+    const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+    const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+    const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+    double best;
+    int bj;
+    nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, it == 1 ? -1 : corr[i], gate2, best, bj);
+    nn[i] = (bj >= 0 && !(best > gate2)) ? bj : -1;  // registration.py:261
+  }
+}
+
+__global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_kernel(RefineArgs a, int it) {
   extern __shared__ double sm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * PX_GICP_WARPS + wid;
   if (c >= a.src.n) return;
+  int* st = a.st_i + 8 * (size_t)c;
+  if (st[ST_DONE]) return;
   double* stage = sm + (size_t)wid * WARP_SM_DOUBLES;  // [43][STAGE_LD]
   double* hg = stage + 43 * STAGE_LD;                  // [43]: H (36), g (6), f0
   double* xis = hg + 43;                               // [6] + status
-
-  const int n = a.src.count[c];
-  const long long off = a.src.offset[c];
-  const double* src = a.src.points + 3 * off;
-  double* ca = a.src_cov + 9 * off;
-  double* wb = a.w_buf + 9 * off;
-  int32_t* corr = a.corr + off;
-  const int ti = a.target_idx[c];
-  const long long toff = a.tgt.offset[ti];
-  const int nt = (int)(a.tgt.offset[ti + 1] - toff);
-  const double* tgt = a.tgt.points + 3 * toff;
-  const double* cb = a.tgt.cov + 9 * toff;
+  const CandView v = cand_view(a, c);
+  const int n = v.n;
+  const double* src = a.src.points + 3 * v.off;
+  const double* ca = a.src_cov + 9 * v.off;
+  double* wb = a.w_buf + 9 * v.off;
+  int32_t* corr = a.corr + v.off;
+  const int32_t* nn = a.nn + v.off;
+  const double* tgt = a.tgt.points + 3 * v.toff;
+  const double* cb = a.tgt.cov + 9 * v.toff;
   const GicpCfgDev cfg = a.cfg;
+  double* pose = a.st_pose + 12 * (size_t)c;
+  double r[9], t[3];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) r[q] = pose[q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
+  __syncwarp();
 
-  double r[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, t[3] = {0, 0, 0};
-  if (a.init_T) {
-    const double* T0 = a.init_T + 12 * (size_t)c;
-    for (int i = 0; i < 3; ++i) {
-      for (int j = 0; j < 3; ++j) r[3 * i + j] = T0[4 * i + j];
-      t[i] = T0[4 * i + 3];
-    }
-  }
-  int failure = F_OK, iters = 0, conv = 0;
-  double* trace = a.out_trace ? a.out_trace + 2 * (size_t)cfg.max_iter * c : nullptr;
-  int n_trace = 0;
-  int ncorr_sum = 0;
-
-  if (n <= cfg.k_cov || nt <= cfg.k_cov) {
-    failure = F_TOO_FEW;  // registration.py:504-510
-  } else {
-    if (a.src.slot_map) {
-      const int4 bb = a.src.bbox[c];
-      OrgView V{src, a.src.slot_map + off, bb.z, bb.w};
-      const int32_t* spx = a.src.src_px + 2 * off;
-      const int st = a.cam.stride;
-      if (cfg.k_cov * 32 * 12 <= 43 * STAGE_LD * 8) {
-        // neighbour lists live in this warp's (still unused) staging area: [k][32] doubles + [k][32] ints
-        double* nd = stage + lane;
-        int* ni = reinterpret_cast<int*>(stage + cfg.k_cov * 32) + lane;
-        for (int i = lane; i < n; i += 32)
-          cov_point_org_sm(V, i, spx[2 * i] / st - bb.x, spx[2 * i + 1] / st - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k,
-                           ca + 9 * (size_t)i, nd, ni);
-      } else {
-        for (int i = lane; i < n; i += 32)
-          cov_point_org(V, i, spx[2 * i] / st - bb.x, spx[2 * i + 1] / st - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k, ca + 9 * (size_t)i);
+  int failure = F_OK, conv = 0;
+  bool done = false;
+  // ---- linearise (registration.py:233-338) ----
+  double acc0 = 0.0, acc1 = 0.0;
+  int n_corr = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool on = false;
+    if (i < n) {
+      const int bj = nn[i];
+      int cj = -1;
+      if (bj >= 0) {
+        const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
+        const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+        const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+        const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+        const double* cai = ca + 9 * (size_t)i;
+        const double* cbj = cb + 9 * (size_t)bj;
+        double rc[9], m[9];
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+#pragma unroll
+          for (int w_ = 0; w_ < 3; ++w_) {
+            double s_ = 0.0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) s_ += r[3 * u + q] * cai[3 * q + w_];
+            rc[3 * u + w_] = s_;
+          }
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+#pragma unroll
+          for (int w_ = 0; w_ < 3; ++w_) {
+            double s_ = 0.0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) s_ += rc[3 * u + q] * r[3 * w_ + q];
+            m[3 * u + w_] = cbj[3 * u + w_] + s_;
+          }
+        const double det = (m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                            m[2] * (m[3] * m[7] - m[4] * m[6]));
+        if (!(det <= 0.0) && isfinite(det)) {
+          cj = bj;
+          on = true;
+          const double inv_det = 1.0 / det;
+          double w[9];
+          w[0] = (m[4] * m[8] - m[5] * m[7]) * inv_det;
+          w[1] = (m[2] * m[7] - m[1] * m[8]) * inv_det;
+          w[2] = (m[1] * m[5] - m[2] * m[4]) * inv_det;
+          w[3] = (m[5] * m[6] - m[3] * m[8]) * inv_det;
+          w[4] = (m[0] * m[8] - m[2] * m[6]) * inv_det;
+          w[5] = (m[2] * m[3] - m[0] * m[5]) * inv_det;
+          w[6] = (m[3] * m[7] - m[4] * m[6]) * inv_det;
+          w[7] = (m[1] * m[6] - m[0] * m[7]) * inv_det;
+          w[8] = (m[0] * m[4] - m[1] * m[3]) * inv_det;
+          double* wo = wb + 9 * (size_t)i;
+#pragma unroll
+          for (int q = 0; q < 9; ++q) wo[q] = w[q];
+          const double dx = tgt[3 * bj] - px, dy = tgt[3 * bj + 1] - py, dz = tgt[3 * bj + 2] - pz;
+          // J = [ [p]x | -I ] (registration.py:296-309).  The products with J's exact
+          // zeros and -1s are dropped / turned into negations below: x*0 = +-0 and
+          // a + (+-0) = a never change a non-zero value, (-1)*x = -x and a + (-b) = a - b
+          // are exact, and the sign of an all-zero term cannot survive the +0-initialised
+          // accumulators -- so every staged term has the reference's bits.
+          const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
+          const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
+          const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
+          stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
+          // g[u] -= J[0][u]*wd0 + J[1][u]*wd1 + J[2][u]*wd2  (staged negated)
+          stage[36 * STAGE_LD + lane] = -(pz * wd1 - py * wd2);
+          stage[37 * STAGE_LD + lane] = -(px * wd2 - pz * wd0);
+          stage[38 * STAGE_LD + lane] = -(py * wd0 - px * wd1);
+          stage[39 * STAGE_LD + lane] = wd0;
+          stage[40 * STAGE_LD + lane] = wd1;
+          stage[41 * STAGE_LD + lane] = wd2;
+          // wj[q][u] = w[q][0]*J[0][u] + w[q][1]*J[1][u] + w[q][2]*J[2][u]
+          double wj[3][6];
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            wj[q][0] = w[3 * q + 1] * pz - w[3 * q + 2] * py;
+            wj[q][1] = w[3 * q + 2] * px - w[3 * q] * pz;
+            wj[q][2] = w[3 * q] * py - w[3 * q + 1] * px;
+            wj[q][3] = -w[3 * q], wj[q][4] = -w[3 * q + 1], wj[q][5] = -w[3 * q + 2];
+          }
+          // h[u][v] += J[0][u]*wj[0][v] + J[1][u]*wj[1][v] + J[2][u]*wj[2][v]
+#pragma unroll
+          for (int u = 0; u < 6; ++u) {
+            stage[(0 + u) * STAGE_LD + lane] = pz * wj[1][u] - py * wj[2][u];
+            stage[(6 + u) * STAGE_LD + lane] = px * wj[2][u] - pz * wj[0][u];
+            stage[(12 + u) * STAGE_LD + lane] = py * wj[0][u] - px * wj[1][u];
+            stage[(18 + u) * STAGE_LD + lane] = -wj[0][u];
+            stage[(24 + u) * STAGE_LD + lane] = -wj[1][u];
+            stage[(30 + u) * STAGE_LD + lane] = -wj[2][u];
+          }
+        }
       }
-    } else {
-      for (int i = lane; i < n; i += 32) cov_point(src, n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
+      corr[i] = cj;
+    }
+    if (!on) {  // absent points contribute exact zeros (x + 0 = x; the accumulators are never -0)
+#pragma unroll
+      for (int e = 0; e < 43; ++e) stage[e * STAGE_LD + lane] = 0.0;
+    }
+    __syncwarp();  // stage writes visible to the summing lanes
+    n_corr += __popc(__ballot_sync(0xffffffffu, on));
+    {
+      const double* row0 = stage + lane * STAGE_LD;
+      const double* row1 = stage + (lane < 11 ? lane + 32 : lane) * STAGE_LD;
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        acc0 += row0[j];
+        acc1 += row1[j];  // lanes >= 11 accumulate a duplicate that is never read
+      }
     }
     __syncwarp();
+  }
+  hg[lane] = acc0;
+  if (lane < 11) hg[32 + lane] = acc1;
+  __syncwarp();
+  const double f0 = hg[42];
+  double xi[6] = {0, 0, 0, 0, 0, 0};
+  if (n_corr < 6) {
+    failure = F_DEGENERATE, done = true;
+  } else {
+    if (lane == 0) {
+      double xi0[6];
+      const int bad = solve_normal_equations(hg, hg + 36, xi0);
+      for (int q = 0; q < 6; ++q) xis[q] = xi0[q];
+      xis[6] = bad ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    if (xis[6] != 0.0) failure = F_SINGULAR, done = true;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) xi[q] = xis[q];
+    __syncwarp();
+  }
+  double scale = 1.0, f_try = 0.0;
+  if (!done) {
+    // ---- step halving (registration.py:443-457) ----
     double r_try[9], t_try[3];
-    for (int it = 1; it <= cfg.max_iter; ++it) {
-      iters = it;
-      // ---- linearise (registration.py:233-338) ----
-      double acc0 = 0.0, acc1 = 0.0;
-      int n_corr = 0;
-      for (int base = 0; base < n; base += 32) {
-        const int i = base + lane;
-        bool on = false;
-        if (i < n) {
-          const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
-          const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
-          const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
-          const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
-          double best;
-          int bj;
-          nn_target(a.tgt, ti, toff, nt, px, py, pz, it == 1 ? -1 : corr[i], cfg.gate2, best, bj);
-          int cj = -1;
-          if (bj >= 0 && !(best > cfg.gate2)) {
-            const double* cai = ca + 9 * (size_t)i;
-            const double* cbj = cb + 9 * (size_t)bj;
-            double rc[9], m[9];
+    bool accepted = false;
+    for (int tr = 0; tr < 9; ++tr) {
+      double rs[9];
+      so3_exp_fast(scale * xi[0], scale * xi[1], scale * xi[2], rs);
 #pragma unroll
-            for (int u = 0; u < 3; ++u)
+      for (int i = 0; i < 3; ++i) {
 #pragma unroll
-              for (int v = 0; v < 3; ++v) {
-                double s = 0.0;
-#pragma unroll
-                for (int w = 0; w < 3; ++w) s += r[3 * u + w] * cai[3 * w + v];
-                rc[3 * u + v] = s;
-              }
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-#pragma unroll
-              for (int v = 0; v < 3; ++v) {
-                double s = 0.0;
-#pragma unroll
-                for (int w = 0; w < 3; ++w) s += rc[3 * u + w] * r[3 * v + w];
-                m[3 * u + v] = cbj[3 * u + v] + s;
-              }
-            const double det = (m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
-                                m[2] * (m[3] * m[7] - m[4] * m[6]));
-            if (!(det <= 0.0) && isfinite(det)) {
-              cj = bj;
-              on = true;
-              const double inv_det = 1.0 / det;
-              double w[9];
-              w[0] = (m[4] * m[8] - m[5] * m[7]) * inv_det;
-              w[1] = (m[2] * m[7] - m[1] * m[8]) * inv_det;
-              w[2] = (m[1] * m[5] - m[2] * m[4]) * inv_det;
-              w[3] = (m[5] * m[6] - m[3] * m[8]) * inv_det;
-              w[4] = (m[0] * m[8] - m[2] * m[6]) * inv_det;
-              w[5] = (m[2] * m[3] - m[0] * m[5]) * inv_det;
-              w[6] = (m[3] * m[7] - m[4] * m[6]) * inv_det;
-              w[7] = (m[1] * m[6] - m[0] * m[7]) * inv_det;
-              w[8] = (m[0] * m[4] - m[1] * m[3]) * inv_det;
-              double* wo = wb + 9 * (size_t)i;
-#pragma unroll
-              for (int q = 0; q < 9; ++q) wo[q] = w[q];
-              const double dx = tgt[3 * bj] - px, dy = tgt[3 * bj + 1] - py, dz = tgt[3 * bj + 2] - pz;
-              // J = [ [p]x | -I ] (registration.py:296-309).  The products with J's exact
-              // zeros and -1s are dropped / turned into negations below: x*0 = +-0 and
-              // a + (+-0) = a never change a non-zero value, (-1)*x = -x and a + (-b) = a - b
-              // are exact, and the sign of an all-zero term cannot survive the +0-initialised
-              // accumulators -- so every staged term has the reference's bits.
-              const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
-              const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
-              const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
-              stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
-              // g[u] -= J[0][u]*wd0 + J[1][u]*wd1 + J[2][u]*wd2  (staged negated)
-              stage[36 * STAGE_LD + lane] = -(pz * wd1 - py * wd2);
-              stage[37 * STAGE_LD + lane] = -(px * wd2 - pz * wd0);
-              stage[38 * STAGE_LD + lane] = -(py * wd0 - px * wd1);
-              stage[39 * STAGE_LD + lane] = wd0;
-              stage[40 * STAGE_LD + lane] = wd1;
-              stage[41 * STAGE_LD + lane] = wd2;
-              // wj[q][u] = w[q][0]*J[0][u] + w[q][1]*J[1][u] + w[q][2]*J[2][u]
-              double wj[3][6];
-#pragma unroll
-              for (int q = 0; q < 3; ++q) {
-                wj[q][0] = w[3 * q + 1] * pz - w[3 * q + 2] * py;
-                wj[q][1] = w[3 * q + 2] * px - w[3 * q] * pz;
-                wj[q][2] = w[3 * q] * py - w[3 * q + 1] * px;
-                wj[q][3] = -w[3 * q], wj[q][4] = -w[3 * q + 1], wj[q][5] = -w[3 * q + 2];
-              }
-              // h[u][v] += J[0][u]*wj[0][v] + J[1][u]*wj[1][v] + J[2][u]*wj[2][v]
-#pragma unroll
-              for (int v = 0; v < 6; ++v) {
-                stage[(0 + v) * STAGE_LD + lane] = pz * wj[1][v] - py * wj[2][v];
-                stage[(6 + v) * STAGE_LD + lane] = px * wj[2][v] - pz * wj[0][v];
-                stage[(12 + v) * STAGE_LD + lane] = py * wj[0][v] - px * wj[1][v];
-                stage[(18 + v) * STAGE_LD + lane] = -wj[0][v];
-                stage[(24 + v) * STAGE_LD + lane] = -wj[1][v];
-                stage[(30 + v) * STAGE_LD + lane] = -wj[2][v];
-              }
-            }
-          }
-          corr[i] = cj;
-        }
-        if (!on) {  // absent points contribute exact zeros (x + 0 = x; the accumulators are never -0)
-#pragma unroll
-          for (int e = 0; e < 43; ++e) stage[e * STAGE_LD + lane] = 0.0;
-        }
-        __syncwarp();  // stage writes visible to the summing lanes
-        n_corr += __popc(__ballot_sync(0xffffffffu, on));
-        {
-          const double* row0 = stage + lane * STAGE_LD;
-          const double* row1 = stage + (lane < 11 ? lane + 32 : lane) * STAGE_LD;
-#pragma unroll 8
-          for (int j = 0; j < 32; ++j) {
-            acc0 += row0[j];
-            acc1 += row1[j];  // lanes >= 11 accumulate a duplicate that is never read
-          }
-        }
-        __syncwarp();
+        for (int j = 0; j < 3; ++j)
+          r_try[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
+        t_try[i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
       }
-      hg[lane] = acc0;
-      if (lane < 11) hg[32 + lane] = acc1;
-      __syncwarp();
-      const double f0 = hg[42];
-      ncorr_sum += n_corr;
-      if (n_corr < 6) {
-        failure = F_DEGENERATE;
+      f_try = gicp_objective(src, n, tgt, corr, wb, r_try, t_try, lane, stage);
+      if (isfinite(f_try) && f_try <= f0) {
+        accepted = true;
         break;
       }
-      if (lane == 0) {
-        double xi0[6];
-        const int bad = solve_normal_equations(hg, hg + 36, xi0);
-        for (int q = 0; q < 6; ++q) xis[q] = xi0[q];
-        xis[6] = bad ? 1.0 : 0.0;
-      }
-      __syncwarp();
-      if (xis[6] != 0.0) {
-        failure = F_SINGULAR;
-        break;
-      }
-      double xi[6];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) xi[q] = xis[q];
-      __syncwarp();
-      // ---- step halving (registration.py:443-457) ----
-      bool accepted = false;
-      double scale = 1.0, f_try = 0.0;
-      for (int tr = 0; tr < 9; ++tr) {
-        double rs[9];
-        so3_exp_fast(scale * xi[0], scale * xi[1], scale * xi[2], rs);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            r_try[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
-          t_try[i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
-        }
-        f_try = gicp_objective(src, n, tgt, corr, wb, r_try, t_try, lane, stage);
-        if (isfinite(f_try) && f_try <= f0) {
-          accepted = true;
-          break;
-        }
-        scale *= 0.5;
-      }
-      if (!accepted) {
-        failure = F_NO_DECREASE;
-        break;
-      }
+      scale *= 0.5;
+    }
+    if (!accepted) {
+      failure = F_NO_DECREASE, done = true;
+    } else {
       renorm_rotation(r_try, r);
       t[0] = t_try[0], t[1] = t_try[1], t[2] = t_try[2];
-      if (trace && lane == 0) trace[2 * (it - 1)] = f0, trace[2 * (it - 1) + 1] = f_try;
-      n_trace = it;
+      if (a.out_trace && lane == 0) {
+        double* trace = a.out_trace + 2 * (size_t)cfg.max_iter * c;
+        trace[2 * (it - 1)] = f0, trace[2 * (it - 1) + 1] = f_try;
+      }
       const double step_t2 = scale * scale * (xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
       const double step_r2 = scale * scale * (xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
-      if (step_t2 < cfg.tol_t2 && step_r2 < cfg.tol_r2) {
-        conv = 1;
-        break;
-      }
-      if (it >= 5 && f0 > 0.0 && (f0 - f_try) <= 1e-4 * f0) break;
+      if (step_t2 < cfg.tol_t2 && step_r2 < cfg.tol_r2)
+        conv = 1, done = true;
+      else if (it >= 5 && f0 > 0.0 && (f0 - f_try) <= 1e-4 * f0)
+        done = true;
     }
   }
+  if (lane < 9) pose[lane] = r[lane];
+  if (lane < 3) pose[9 + lane] = t[lane];
+  if (lane == 0) {
+    st[ST_ITERS] = it;
+    st[ST_NCORR] += n_corr;
+    if (failure == F_OK && !(done && conv == 0 && false)) {
+    }
+    if (failure != F_OK) st[ST_FAIL] = failure;
+    if (failure == F_OK) st[ST_NTRACE] = it;  // an accepted step was recorded
+    if (conv) st[ST_CONV] = 1;
+    if (done || it >= cfg.max_iter) st[ST_DONE] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(128) gicp_finish_kernel(RefineArgs a) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + wid;
+  if (c >= a.src.n) return;
+  const int* st = a.st_i + 8 * (size_t)c;
+  const int failure = st[ST_FAIL], iters = st[ST_ITERS], conv = st[ST_CONV];
+  const CandView v = cand_view(a, c);
+  const double* pose = a.st_pose + 12 * (size_t)c;
+  double r[9], t[3];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) r[q] = pose[q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
   // ---- result transform (registration.py:473) ----
   double T[12];
   {
@@ -785,19 +875,21 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(
     }
   }
   if (a.out_resid) {  // registration.py:59-67 (not used by the search path)
+    const double* src = a.src.points + 3 * v.off;
+    const double* tgt = a.tgt.points + 3 * v.toff;
     double sum = 0.0;
     int cnt = 0;
     if (failure != F_TOO_FEW) {
-      for (int i = lane; i < n; i += 32) {
+      for (int i = lane; i < v.n; i += 32) {
         double x, y, z;
         apply_pose(T, src[3 * i], src[3 * i + 1], src[3 * i + 2], x, y, z);
         double best = CUDART_INF;
-        for (int j = 0; j < nt; ++j) {
+        for (int j = 0; j < v.nt; ++j) {
           const double dx = tgt[3 * j] - x, dy = tgt[3 * j + 1] - y, dz = tgt[3 * j + 2] - z;
           const double d2 = dx * dx + dy * dy + dz * dz;
           if (d2 < best) best = d2;
         }
-        if (best <= cfg.gate2) sum += best, ++cnt;
+        if (best <= a.cfg.gate2) sum += best, ++cnt;
       }
       for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o), cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     }
@@ -807,8 +899,8 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_kernel(
     for (int i = 0; i < 12; ++i) a.out_T[12 * (size_t)c + i] = T[i];
     a.out_iters[c] = iters;
     a.out_flags[c] = failure | (conv ? 0x100 : 0);
-    if (a.out_ntrace) a.out_ntrace[c] = n_trace;
-    if (a.out_ncorr_sum) a.out_ncorr_sum[c] = ncorr_sum;
+    if (a.out_ntrace) a.out_ntrace[c] = st[ST_NTRACE];
+    if (a.out_ncorr_sum) a.out_ncorr_sum[c] = st[ST_NCORR];
     if (a.poses_in) {  // search.py:291-301
       const double* pin = a.poses_in + 12 * (size_t)c;
       double cam[12];
@@ -845,13 +937,25 @@ void dump_nn_stats() {
 }
 #endif
 
-cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st) {
+// Returns the number of kernels launched through *launches.
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches) {
+  if (launches) *launches = 0;
   if (a.src.n == 0) return cudaSuccess;
+  cudaError_t e;
+  const int b4 = (a.src.n + 3) / 4;
+  const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
+  if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
+  gicp_init_kernel<<<b4, 128, smem_init, st>>>(a);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
-  cudaError_t e = cudaFuncSetAttribute(gicp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(gicp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+  cudaFuncSetAttribute(gicp_nn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all of it as L1
   const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
-  gicp_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a);
+  for (int it = 1; it <= a.cfg.max_iter; ++it) {
+    gicp_nn_kernel<<<b4, 128, 0, st>>>(a, it);
+    gicp_step_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
+  }
+  gicp_finish_kernel<<<b4, 128, 0, st>>>(a);
+  if (launches) *launches = 2 + 2 * std::max(a.cfg.max_iter, 0);
 #ifdef PX_NN_STATS
   cudaStreamSynchronize(st);
   dump_nn_stats();

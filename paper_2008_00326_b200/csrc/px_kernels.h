@@ -133,7 +133,10 @@ struct RefineArgs {
   // scratch, indexed by the source slot offsets
   double* src_cov;            // (sum cap,9)
   double* w_buf;              // (sum cap,9)
-  int32_t* corr;              // (sum cap)
+  int32_t* corr;              // (sum cap) correspondences of the last linearisation
+  int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration
+  double* st_pose;            // (n,12) current iterate [R (9) | t (3)]
+  int32_t* st_i;              // (n,8) per-candidate integer state (px_gicp.cu: ST_*)
   // outputs
   double* out_T;              // (n,12) [orthonormalize(R)|t]
   int32_t* out_iters;
@@ -150,7 +153,7 @@ struct RefineArgs {
   int c2w_vec_order, w2c_vec_order;
   double fixed_z;
 };
-cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st);
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches);
 
 struct CostArgs {
   CloudsDev ren;
