@@ -82,7 +82,7 @@ struct px_ctx {
   long long tgt_total = 0;
   int tgt_k = 0;
   double tgt_gate = 0.0;
-  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
+  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
   bool tgt_organised = false;
   // resident candidates
   int64_t n_cand = 0;
@@ -91,6 +91,7 @@ struct px_ctx {
   // search scratch / results
   CloudStore clouds;
   DevBuf src_cov, w_buf, corr, nn, st_pose, st_i, total_dev;
+  long long refine_plane = 0;  // plane stride of the structure-of-arrays refine scratch
   DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1;
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
@@ -280,10 +281,11 @@ int check_gicp(px_ctx* ctx, const px_gicp_cfg& g) {
 int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   size_t tot = (size_t)std::max<long long>(total_cap, 1);
   CU(ctx->nn.ensure(sizeof(int32_t) * tot));
-  CU(ctx->st_pose.ensure(sizeof(double) * 12 * (size_t)std::max<int64_t>(n_cand, 1)));
+  CU(ctx->st_pose.ensure(sizeof(double) * 20 * (size_t)std::max<int64_t>(n_cand, 1)));
   CU(ctx->st_i.ensure(sizeof(int32_t) * 8 * (size_t)std::max<int64_t>(n_cand, 1)));
+  ctx->refine_plane = (long long)tot;
   CU(ctx->src_cov.ensure(sizeof(double) * 9 * tot));
-  CU(ctx->w_buf.ensure(sizeof(double) * 9 * tot));
+  CU(ctx->w_buf.ensure(sizeof(double) * 15 * tot));
   CU(ctx->corr.ensure(sizeof(int32_t) * tot));
   return 0;
 }
@@ -329,7 +331,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
-                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
+                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
@@ -671,6 +673,8 @@ static TargetsDev targets_dev(px_ctx* ctx) {
   t.boxes32 = ctx->tgt_boxes.as<float>();
   t.leaf_start = ctx->tgt_lstart.as<int32_t>();
   t.leaf32 = ctx->tgt_lpts.as<float4>();
+  t.soa = ctx->tgt_soa.as<double>();
+  t.plane = std::max<long long>(ctx->tgt_total, 1);
   return t;
 }
 
@@ -826,7 +830,9 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     if (org) a.org = ctx->tgt_org.as<TgtOrg>(), a.tmap = ctx->tgt_map.as<int32_t>(), a.tpix = ctx->tgt_pix.as<int32_t>();
     a.ray_k = ctx->cam.ray_k;
     CU(launch_cov(a, total, ctx->stream));
-    ctx->launches += 1;
+    CU(ctx->tgt_soa.ensure(tot1 * 72));
+    CU(launch_soa(ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
+    ctx->launches += 2;
   }
   CU(cudaStreamSynchronize(ctx->stream));  // host staging vectors are stack-owned
   return 0;
@@ -870,7 +876,8 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
     a.init_T = init_T ? dinit.as<double>() : nullptr;
     a.cfg = gicp_dev(*cfg);
     a.cam = ctx->cam;
-    a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.plane = ctx->refine_plane;
     a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
     a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
     a.out_resid = out_residual ? dres.as<double>() : nullptr;
@@ -1029,7 +1036,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   long long total = 0;
   if (timed) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (int r = size_clouds(ctx, ctx->clouds, slot, pose_in, n, &total)) return r;
-  const long long per_slot = 60 + (cfg->refine ? 152 : 0);
+  const long long per_slot = 60 + (cfg->refine ? 200 : 0);
   if (total * per_slot > ctx->scratch_budget && n > 1024) {
     const int64_t mid = lo + n / 2;
     if (int r = search_range(ctx, cfg, lo, mid)) return r;
@@ -1048,7 +1055,8 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     a.target_idx = ctx->c_tidx.as<int32_t>() + lo;
     a.cfg = gicp_dev(cfg->gicp);
     a.cam = ctx->cam;
-    a.src_cov = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.plane = ctx->refine_plane;
     a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
     a.out_T = ctx->r_T.as<double>() + 12 * lo;
     a.out_iters = ctx->r_iters.as<int32_t>() + lo, a.out_flags = ctx->r_flags.as<int32_t>() + lo;

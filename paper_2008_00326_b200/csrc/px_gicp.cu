@@ -270,6 +270,21 @@ cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void soa_kernel(const double* __restrict__ pts, const double* __restrict__ cov, double* __restrict__ soa, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* c = cov + 9 * i;
+  soa[i] = pts[3 * i], soa[n + i] = pts[3 * i + 1], soa[2 * n + i] = pts[3 * i + 2];
+  soa[3 * n + i] = c[0], soa[4 * n + i] = c[1], soa[5 * n + i] = c[2];
+  soa[6 * n + i] = c[4], soa[7 * n + i] = c[5], soa[8 * n + i] = c[8];
+}
+
+cudaError_t launch_soa(const double* pts, const double* cov, double* soa, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  soa_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pts, cov, soa, n);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // Exact nearest neighbour over an organised target with a two-level box
 // hierarchy in image space: blocks of PX_BLK x PX_BLK map cells and super-blocks
@@ -281,7 +296,11 @@ cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
 // monotone), so no candidate is ever skipped.
 
 #ifdef PX_NN_STATS
-__device__ unsigned long long g_nn_stats[8];  // queries, with-prev, sb tests, blk tests, leaf pts, found, leaves opened
+__device__ unsigned long long g_nn_stats[8];
+__device__ unsigned long long g_nn_rhist[8];
+__device__ double g_nn_rayk;
+__device__ float* g_nn_prevq;
+__device__ unsigned long long g_nn_mhist[8];  // queries, with-prev, sb tests, blk tests, leaf pts, found, leaves opened
 #define NN_STAT(i, v) atomicAdd(&g_nn_stats[i], (unsigned long long)(v))
 #else
 #define NN_STAT(i, v)
@@ -391,6 +410,16 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
       }
     if (bj == 0x7fffffff) best = CUDART_INF, bj = -1;
     NN_STAT(5, bj >= 0);
+#ifdef PX_NN_STATS
+    {
+      int b_ = 7;
+      if (bj >= 0) {
+        const double R = sqrt(best) / (qz * g_nn_rayk);
+        b_ = R < 0.5 ? 0 : R < 1.5 ? 1 : R < 2.5 ? 2 : R < 3.5 ? 3 : R < 5.5 ? 4 : R < 8.5 ? 5 : 6;
+      }
+      atomicAdd(&g_nn_rhist[b_], 1ull);
+    }
+#endif
     return;
   }
   // generic clouds: the reference's linear scan
@@ -505,32 +534,33 @@ __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync
 // fixed-association objective, registration.py:387-407; uniform result in all lanes.
 // Per-point terms are written to `sbuf` (32 doubles of shared memory per warp) and
 // every lane adds them in source-index order (absent points add an exact +0).
-__device__ double gicp_objective(const double* __restrict__ src, int n, const double* __restrict__ tgt,
-                                 const int32_t* __restrict__ corr, const double* __restrict__ wb,
-                                 const double* r, const double* t, int lane, double* sbuf) {
+__device__ __forceinline__ double gicp_objective(const double* __restrict__ wb, long long plane, int nc, const double* r,
+                                                 const double* t, int lane, double* sbuf) {
   double f = 0.0;
-  for (int base = 0; base < n; base += 32) {
-    const int i = base + lane;
+  for (int base = 0; base < nc; base += 32) {
+    const int k = base + lane;
     double term = 0.0;
-    if (i < n) {
-      const int j = corr[i];
-      if (j >= 0) {
-        const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
-        const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
-        const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
-        const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
-        const double dx = tgt[3 * j] - px, dy = tgt[3 * j + 1] - py, dz = tgt[3 * j + 2] - pz;
-        const double* w = wb + 9 * (size_t)i;
-        const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
-        const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
-        const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
-        term = dx * wd0 + dy * wd1 + dz * wd2;
-      }
+    if (k < nc) {
+      const double* w = wb + k;
+      const double ax = w[9 * plane], ay = w[10 * plane], az = w[11 * plane];
+      const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+      const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+      const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+      const double dx = w[12 * plane] - px, dy = w[13 * plane] - py, dz = w[14 * plane] - pz;
+      const double wd0 = w[0] * dx + w[plane] * dy + w[2 * plane] * dz;
+      const double wd1 = w[3 * plane] * dx + w[4 * plane] * dy + w[5 * plane] * dz;
+      const double wd2 = w[6 * plane] * dx + w[7 * plane] * dy + w[8 * plane] * dz;
+      term = dx * wd0 + dy * wd1 + dz * wd2;
     }
     sbuf[lane] = term;
     __syncwarp();
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) f += sbuf[j];
+    const double2* s2 = reinterpret_cast<const double2*>(sbuf);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double2 v = s2[j];
+      f += v.x;
+      f += v.y;
+    }
     __syncwarp();
   }
   return f;
@@ -553,7 +583,11 @@ __device__ double gicp_objective(const double* __restrict__ src, int n, const do
 // where the loop counter lives changed.
 
 // per-candidate integer state (RefineArgs::st_i, 8 ints each)
-enum { ST_FAIL = 0, ST_DONE = 1, ST_ITERS = 2, ST_CONV = 3, ST_NTRACE = 4, ST_NCORR = 5 };
+enum { ST_FAIL = 0, ST_DONE = 1, ST_ITERS = 2, ST_CONV = 3, ST_NTRACE = 4, ST_NCORR = 5, ST_NCOMPACT = 6 };
+#define ST_POSE_LD 20  // per-candidate double state: R (9), t (3), xi (6), f0, pad
+#ifndef PX_HALVE_MINB
+#define PX_HALVE_MINB 6
+#endif
 
 struct CandView {
   int n, nt, ti;
@@ -569,17 +603,25 @@ __device__ __forceinline__ CandView cand_view(const RefineArgs& a, int c) {
   return v;
 }
 
+// the covariance is bit-symmetric (registration.py:211-216 writes v0 v0^T entry by entry with commuting products)
+__device__ __forceinline__ void store_src_soa(double* soa, long long plane, int i, const double* src, const double* cv) {
+  soa[i] = src[3 * i], soa[plane + i] = src[3 * i + 1], soa[2 * plane + i] = src[3 * i + 2];
+  soa[3 * plane + i] = cv[0], soa[4 * plane + i] = cv[1], soa[5 * plane + i] = cv[2];
+  soa[6 * plane + i] = cv[4], soa[7 * plane + i] = cv[5], soa[8 * plane + i] = cv[8];
+}
+
 __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
-  extern __shared__ double sm[];  // per warp: [k][32] doubles + [k][32] ints of neighbour lists
+  extern __shared__ __align__(16) double sm[];  // per warp: [k][32] doubles + [k][32] ints of neighbour lists
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + wid;
   if (c >= a.src.n) return;
   const CandView v = cand_view(a, c);
   const GicpCfgDev cfg = a.cfg;
   const double* src = a.src.points + 3 * v.off;
-  double* ca = a.src_cov + 9 * v.off;
+  double* soa = a.src_soa + v.off;  // planes x, y, z, c00, c01, c02, c11, c12, c22
+  const long long plane = a.plane;
   int* st = a.st_i + 8 * (size_t)c;
-  double* pose = a.st_pose + 12 * (size_t)c;
+  double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
   if (lane < 12) {
     double val = (lane == 0 || lane == 4 || lane == 8) ? 1.0 : 0.0;  // [R | t] as 9 + 3
     if (a.init_T) {
@@ -598,11 +640,17 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
     const int stp = a.cam.stride;
     double* nd = sm + (size_t)wid * (cfg.k_cov * 48) + lane;
     int* ni = reinterpret_cast<int*>(sm + (size_t)wid * (cfg.k_cov * 48) + cfg.k_cov * 32) + lane;
-    for (int i = lane; i < v.n; i += 32)
-      cov_point_org_sm(V, i, spx[2 * i] / stp - bb.x, spx[2 * i + 1] / stp - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k,
-                       ca + 9 * (size_t)i, nd, ni);
+    for (int i = lane; i < v.n; i += 32) {
+      double cv[9];
+      cov_point_org_sm(V, i, spx[2 * i] / stp - bb.x, spx[2 * i + 1] / stp - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k, cv, nd, ni);
+      store_src_soa(soa, plane, i, src, cv);
+    }
   } else {
-    for (int i = lane; i < v.n; i += 32) cov_point(src, v.n, i, cfg.k_cov, cfg.eps, ca + 9 * (size_t)i);
+    for (int i = lane; i < v.n; i += 32) {
+      double cv[9];
+      cov_point(src, v.n, i, cfg.k_cov, cfg.eps, cv);
+      store_src_soa(soa, plane, i, src, cv);
+    }
   }
 }
 
@@ -612,17 +660,18 @@ __global__ void __launch_bounds__(128, 8) gicp_nn_kernel(RefineArgs a, int it) {
   if (c >= a.src.n) return;
   if (a.st_i[8 * (size_t)c + ST_DONE]) return;
   const CandView v = cand_view(a, c);
-  const double* src = a.src.points + 3 * v.off;
+  const double* soa = a.src_soa + v.off;
+  const long long plane = a.plane;
   const int32_t* corr = a.corr + v.off;
   int32_t* nn = a.nn + v.off;
   double r[9], t[3];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) r[q] = a.st_pose[12 * (size_t)c + q];
+  for (int q = 0; q < 9; ++q) r[q] = a.st_pose[ST_POSE_LD * (size_t)c + q];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) t[q] = a.st_pose[12 * (size_t)c + 9 + q];
+  for (int q = 0; q < 3; ++q) t[q] = a.st_pose[ST_POSE_LD * (size_t)c + 9 + q];
   const double gate2 = a.cfg.gate2;
   for (int i = lane; i < v.n; i += 32) {
-    const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
+    const double ax = soa[i], ay = soa[plane + i], az = soa[2 * plane + i];
     const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
     const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
     const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
@@ -630,11 +679,28 @@ __global__ void __launch_bounds__(128, 8) gicp_nn_kernel(RefineArgs a, int it) {
     int bj;
     nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, it == 1 ? -1 : corr[i], gate2, best, bj);
     nn[i] = (bj >= 0 && !(best > gate2)) ? bj : -1;  // registration.py:261
+#ifdef PX_NN_STATS
+    {
+      float* pq = g_nn_prevq + 3 * (v.off + i);
+      if (it > 1) {
+        const double mx = px - pq[0], my = py - pq[1], mz = pz - pq[2];
+        const double m = sqrt(mx * mx + my * my + mz * mz) * 1e3;  // mm
+        const int b_ = m < 0.03 ? 0 : m < 0.1 ? 1 : m < 0.3 ? 2 : m < 1.0 ? 3 : m < 3.0 ? 4 : m < 10.0 ? 5 : 6;
+        atomicAdd(&g_nn_mhist[b_], 1ull);
+      }
+      pq[0] = (float)px, pq[1] = (float)py, pq[2] = (float)pz;
+    }
+#endif
   }
 }
 
-__global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_kernel(RefineArgs a, int it) {
-  extern __shared__ double sm[];
+// Linearisation (registration.py:233-338) for iteration `it`: per-point terms lane-parallel, staged
+// through shared memory and summed in source-index order by 43 lanes; then the 6x6 solve.
+// Matched points are compacted (in index order) into 15 planes {W (9), source point (3), target
+// point (3)} for the step-halving kernel, whose objective visits exactly the matched points in
+// ascending index order (registration.py:387-407).
+__global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_kernel(RefineArgs a, int it) {
+  extern __shared__ __align__(16) double sm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * PX_GICP_WARPS + wid;
   if (c >= a.src.n) return;
@@ -642,127 +708,130 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_ke
   if (st[ST_DONE]) return;
   double* stage = sm + (size_t)wid * WARP_SM_DOUBLES;  // [43][STAGE_LD]
   double* hg = stage + 43 * STAGE_LD;                  // [43]: H (36), g (6), f0
-  double* xis = hg + 43;                               // [6] + status
   const CandView v = cand_view(a, c);
   const int n = v.n;
-  const double* src = a.src.points + 3 * v.off;
-  const double* ca = a.src_cov + 9 * v.off;
-  double* wb = a.w_buf + 9 * v.off;
+  const double* soa = a.src_soa + v.off;  // planes x, y, z, c00, c01, c02, c11, c12, c22
+  const long long plane = a.plane;
+  double* wb = a.w_buf + v.off;           // 15 compact planes
   int32_t* corr = a.corr + v.off;
   const int32_t* nn = a.nn + v.off;
-  const double* tgt = a.tgt.points + 3 * v.toff;
-  const double* cb = a.tgt.cov + 9 * v.toff;
-  const GicpCfgDev cfg = a.cfg;
-  double* pose = a.st_pose + 12 * (size_t)c;
+  const double* tsoa = a.tgt.soa + v.toff;  // same nine planes of the target
+  const long long tplane = a.tgt.plane;
+  double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
   double r[9], t[3];
 #pragma unroll
   for (int q = 0; q < 9; ++q) r[q] = pose[q];
 #pragma unroll
   for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
-  __syncwarp();
 
-  int failure = F_OK, conv = 0;
-  bool done = false;
-  // ---- linearise (registration.py:233-338) ----
   double acc0 = 0.0, acc1 = 0.0;
   int n_corr = 0;
+  int bj_next = lane < n ? nn[lane] : -1;
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
+    const int bj = bj_next;
+    bj_next = i + 32 < n ? nn[i + 32] : -1;  // next chunk's neighbours are in flight during this chunk
     bool on = false;
-    if (i < n) {
-      const int bj = nn[i];
-      int cj = -1;
-      if (bj >= 0) {
-        const double ax = src[3 * i], ay = src[3 * i + 1], az = src[3 * i + 2];
-        const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
-        const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
-        const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
-        const double* cai = ca + 9 * (size_t)i;
-        const double* cbj = cb + 9 * (size_t)bj;
-        double rc[9], m[9];
+    double w[9], ax = 0, ay = 0, az = 0, tx = 0, ty = 0, tz = 0;
+    if (bj >= 0) {
+      ax = soa[i], ay = soa[plane + i], az = soa[2 * plane + i];
+      tx = tsoa[bj], ty = tsoa[tplane + bj], tz = tsoa[2 * tplane + bj];
+      const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+      const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+      const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+      double cai[9], cbj[9];
+      cai[0] = soa[3 * plane + i], cai[1] = soa[4 * plane + i], cai[2] = soa[5 * plane + i];
+      cai[4] = soa[6 * plane + i], cai[5] = soa[7 * plane + i], cai[8] = soa[8 * plane + i];
+      cai[3] = cai[1], cai[6] = cai[2], cai[7] = cai[5];
+      cbj[0] = tsoa[3 * tplane + bj], cbj[1] = tsoa[4 * tplane + bj], cbj[2] = tsoa[5 * tplane + bj];
+      cbj[4] = tsoa[6 * tplane + bj], cbj[5] = tsoa[7 * tplane + bj], cbj[8] = tsoa[8 * tplane + bj];
+      cbj[3] = cbj[1], cbj[6] = cbj[2], cbj[7] = cbj[5];
+      double rc[9], m[9];
 #pragma unroll
-        for (int u = 0; u < 3; ++u)
+      for (int u = 0; u < 3; ++u)
 #pragma unroll
-          for (int w_ = 0; w_ < 3; ++w_) {
-            double s_ = 0.0;
+        for (int w_ = 0; w_ < 3; ++w_) {
+          double s_ = 0.0;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) s_ += r[3 * u + q] * cai[3 * q + w_];
-            rc[3 * u + w_] = s_;
-          }
+          for (int q = 0; q < 3; ++q) s_ += r[3 * u + q] * cai[3 * q + w_];
+          rc[3 * u + w_] = s_;
+        }
 #pragma unroll
-        for (int u = 0; u < 3; ++u)
+      for (int u = 0; u < 3; ++u)
 #pragma unroll
-          for (int w_ = 0; w_ < 3; ++w_) {
-            double s_ = 0.0;
+        for (int w_ = 0; w_ < 3; ++w_) {
+          double s_ = 0.0;
 #pragma unroll
-            for (int q = 0; q < 3; ++q) s_ += rc[3 * u + q] * r[3 * w_ + q];
-            m[3 * u + w_] = cbj[3 * u + w_] + s_;
-          }
-        const double det = (m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
-                            m[2] * (m[3] * m[7] - m[4] * m[6]));
-        if (!(det <= 0.0) && isfinite(det)) {
-          cj = bj;
-          on = true;
-          const double inv_det = 1.0 / det;
-          double w[9];
-          w[0] = (m[4] * m[8] - m[5] * m[7]) * inv_det;
-          w[1] = (m[2] * m[7] - m[1] * m[8]) * inv_det;
-          w[2] = (m[1] * m[5] - m[2] * m[4]) * inv_det;
-          w[3] = (m[5] * m[6] - m[3] * m[8]) * inv_det;
-          w[4] = (m[0] * m[8] - m[2] * m[6]) * inv_det;
-          w[5] = (m[2] * m[3] - m[0] * m[5]) * inv_det;
-          w[6] = (m[3] * m[7] - m[4] * m[6]) * inv_det;
-          w[7] = (m[1] * m[6] - m[0] * m[7]) * inv_det;
-          w[8] = (m[0] * m[4] - m[1] * m[3]) * inv_det;
-          double* wo = wb + 9 * (size_t)i;
+          for (int q = 0; q < 3; ++q) s_ += rc[3 * u + q] * r[3 * w_ + q];
+          m[3 * u + w_] = cbj[3 * u + w_] + s_;
+        }
+      const double det = (m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                          m[2] * (m[3] * m[7] - m[4] * m[6]));
+      if (!(det <= 0.0) && isfinite(det)) {
+        on = true;
+        const double inv_det = 1.0 / det;
+        w[0] = (m[4] * m[8] - m[5] * m[7]) * inv_det;
+        w[1] = (m[2] * m[7] - m[1] * m[8]) * inv_det;
+        w[2] = (m[1] * m[5] - m[2] * m[4]) * inv_det;
+        w[3] = (m[5] * m[6] - m[3] * m[8]) * inv_det;
+        w[4] = (m[0] * m[8] - m[2] * m[6]) * inv_det;
+        w[5] = (m[2] * m[3] - m[0] * m[5]) * inv_det;
+        w[6] = (m[3] * m[7] - m[4] * m[6]) * inv_det;
+        w[7] = (m[1] * m[6] - m[0] * m[7]) * inv_det;
+        w[8] = (m[0] * m[4] - m[1] * m[3]) * inv_det;
+        const double dx = tx - px, dy = ty - py, dz = tz - pz;
+        // J = [ [p]x | -I ] (registration.py:296-309).  The products with J's exact
+        // zeros and -1s are dropped / turned into negations below: x*0 = +-0 and
+        // a + (+-0) = a never change a non-zero value, (-1)*x = -x and a + (-b) = a - b
+        // are exact, and the sign of an all-zero term cannot survive the +0-initialised
+        // accumulators -- so every staged term has the reference's bits.
+        const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
+        const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
+        const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
+        stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
+        // g[u] -= J[0][u]*wd0 + J[1][u]*wd1 + J[2][u]*wd2  (staged negated)
+        stage[36 * STAGE_LD + lane] = -(pz * wd1 - py * wd2);
+        stage[37 * STAGE_LD + lane] = -(px * wd2 - pz * wd0);
+        stage[38 * STAGE_LD + lane] = -(py * wd0 - px * wd1);
+        stage[39 * STAGE_LD + lane] = wd0;
+        stage[40 * STAGE_LD + lane] = wd1;
+        stage[41 * STAGE_LD + lane] = wd2;
+        // wj[q][u] = w[q][0]*J[0][u] + w[q][1]*J[1][u] + w[q][2]*J[2][u]
+        double wj[3][6];
 #pragma unroll
-          for (int q = 0; q < 9; ++q) wo[q] = w[q];
-          const double dx = tgt[3 * bj] - px, dy = tgt[3 * bj + 1] - py, dz = tgt[3 * bj + 2] - pz;
-          // J = [ [p]x | -I ] (registration.py:296-309).  The products with J's exact
-          // zeros and -1s are dropped / turned into negations below: x*0 = +-0 and
-          // a + (+-0) = a never change a non-zero value, (-1)*x = -x and a + (-b) = a - b
-          // are exact, and the sign of an all-zero term cannot survive the +0-initialised
-          // accumulators -- so every staged term has the reference's bits.
-          const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
-          const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
-          const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
-          stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
-          // g[u] -= J[0][u]*wd0 + J[1][u]*wd1 + J[2][u]*wd2  (staged negated)
-          stage[36 * STAGE_LD + lane] = -(pz * wd1 - py * wd2);
-          stage[37 * STAGE_LD + lane] = -(px * wd2 - pz * wd0);
-          stage[38 * STAGE_LD + lane] = -(py * wd0 - px * wd1);
-          stage[39 * STAGE_LD + lane] = wd0;
-          stage[40 * STAGE_LD + lane] = wd1;
-          stage[41 * STAGE_LD + lane] = wd2;
-          // wj[q][u] = w[q][0]*J[0][u] + w[q][1]*J[1][u] + w[q][2]*J[2][u]
-          double wj[3][6];
+        for (int q = 0; q < 3; ++q) {
+          wj[q][0] = w[3 * q + 1] * pz - w[3 * q + 2] * py;
+          wj[q][1] = w[3 * q + 2] * px - w[3 * q] * pz;
+          wj[q][2] = w[3 * q] * py - w[3 * q + 1] * px;
+          wj[q][3] = -w[3 * q], wj[q][4] = -w[3 * q + 1], wj[q][5] = -w[3 * q + 2];
+        }
+        // h[u][v] += J[0][u]*wj[0][v] + J[1][u]*wj[1][v] + J[2][u]*wj[2][v]
 #pragma unroll
-          for (int q = 0; q < 3; ++q) {
-            wj[q][0] = w[3 * q + 1] * pz - w[3 * q + 2] * py;
-            wj[q][1] = w[3 * q + 2] * px - w[3 * q] * pz;
-            wj[q][2] = w[3 * q] * py - w[3 * q + 1] * px;
-            wj[q][3] = -w[3 * q], wj[q][4] = -w[3 * q + 1], wj[q][5] = -w[3 * q + 2];
-          }
-          // h[u][v] += J[0][u]*wj[0][v] + J[1][u]*wj[1][v] + J[2][u]*wj[2][v]
-#pragma unroll
-          for (int u = 0; u < 6; ++u) {
-            stage[(0 + u) * STAGE_LD + lane] = pz * wj[1][u] - py * wj[2][u];
-            stage[(6 + u) * STAGE_LD + lane] = px * wj[2][u] - pz * wj[0][u];
-            stage[(12 + u) * STAGE_LD + lane] = py * wj[0][u] - px * wj[1][u];
-            stage[(18 + u) * STAGE_LD + lane] = -wj[0][u];
-            stage[(24 + u) * STAGE_LD + lane] = -wj[1][u];
-            stage[(30 + u) * STAGE_LD + lane] = -wj[2][u];
-          }
+        for (int u = 0; u < 6; ++u) {
+          stage[(0 + u) * STAGE_LD + lane] = pz * wj[1][u] - py * wj[2][u];
+          stage[(6 + u) * STAGE_LD + lane] = px * wj[2][u] - pz * wj[0][u];
+          stage[(12 + u) * STAGE_LD + lane] = py * wj[0][u] - px * wj[1][u];
+          stage[(18 + u) * STAGE_LD + lane] = -wj[0][u];
+          stage[(24 + u) * STAGE_LD + lane] = -wj[1][u];
+          stage[(30 + u) * STAGE_LD + lane] = -wj[2][u];
         }
       }
-      corr[i] = cj;
     }
+    if (i < n) corr[i] = on ? bj : -1;
     if (!on) {  // absent points contribute exact zeros (x + 0 = x; the accumulators are never -0)
 #pragma unroll
       for (int e = 0; e < 43; ++e) stage[e * STAGE_LD + lane] = 0.0;
     }
     __syncwarp();  // stage writes visible to the summing lanes
-    n_corr += __popc(__ballot_sync(0xffffffffu, on));
+    const unsigned onm = __ballot_sync(0xffffffffu, on);
+    if (on) {  // ordered compaction for the halving kernel
+      double* o = wb + n_corr + __popc(onm & ((1u << lane) - 1u));
+#pragma unroll
+      for (int q = 0; q < 9; ++q) o[q * plane] = w[q];
+      o[9 * plane] = ax, o[10 * plane] = ay, o[11 * plane] = az;
+      o[12 * plane] = tx, o[13 * plane] = ty, o[14 * plane] = tz;
+    }
+    n_corr += __popc(onm);
     {
       const double* row0 = stage + lane * STAGE_LD;
       const double* row1 = stage + (lane < 11 ? lane + 32 : lane) * STAGE_LD;
@@ -777,69 +846,87 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_ke
   hg[lane] = acc0;
   if (lane < 11) hg[32 + lane] = acc1;
   __syncwarp();
-  const double f0 = hg[42];
-  double xi[6] = {0, 0, 0, 0, 0, 0};
-  if (n_corr < 6) {
-    failure = F_DEGENERATE, done = true;
-  } else {
-    if (lane == 0) {
-      double xi0[6];
-      const int bad = solve_normal_equations(hg, hg + 36, xi0);
-      for (int q = 0; q < 6; ++q) xis[q] = xi0[q];
-      xis[6] = bad ? 1.0 : 0.0;
-    }
-    __syncwarp();
-    if (xis[6] != 0.0) failure = F_SINGULAR, done = true;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) xi[q] = xis[q];
-    __syncwarp();
-  }
-  double scale = 1.0, f_try = 0.0;
-  if (!done) {
-    // ---- step halving (registration.py:443-457) ----
-    double r_try[9], t_try[3];
-    bool accepted = false;
-    for (int tr = 0; tr < 9; ++tr) {
-      double rs[9];
-      so3_exp_fast(scale * xi[0], scale * xi[1], scale * xi[2], rs);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          r_try[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
-        t_try[i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
-      }
-      f_try = gicp_objective(src, n, tgt, corr, wb, r_try, t_try, lane, stage);
-      if (isfinite(f_try) && f_try <= f0) {
-        accepted = true;
-        break;
-      }
-      scale *= 0.5;
-    }
-    if (!accepted) {
-      failure = F_NO_DECREASE, done = true;
-    } else {
-      renorm_rotation(r_try, r);
-      t[0] = t_try[0], t[1] = t_try[1], t[2] = t_try[2];
-      if (a.out_trace && lane == 0) {
-        double* trace = a.out_trace + 2 * (size_t)cfg.max_iter * c;
-        trace[2 * (it - 1)] = f0, trace[2 * (it - 1) + 1] = f_try;
-      }
-      const double step_t2 = scale * scale * (xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
-      const double step_r2 = scale * scale * (xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
-      if (step_t2 < cfg.tol_t2 && step_r2 < cfg.tol_r2)
-        conv = 1, done = true;
-      else if (it >= 5 && f0 > 0.0 && (f0 - f_try) <= 1e-4 * f0)
-        done = true;
-    }
-  }
-  if (lane < 9) pose[lane] = r[lane];
-  if (lane < 3) pose[9 + lane] = t[lane];
   if (lane == 0) {
+    int failure = F_OK;
+    double xi0[6] = {0, 0, 0, 0, 0, 0};
+    if (n_corr < 6)
+      failure = F_DEGENERATE;
+    else if (solve_normal_equations(hg, hg + 36, xi0))
+      failure = F_SINGULAR;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) pose[12 + q] = xi0[q];
+    pose[18] = hg[42];
     st[ST_ITERS] = it;
     st[ST_NCORR] += n_corr;
-    if (failure == F_OK && !(done && conv == 0 && false)) {
+    st[ST_NCOMPACT] = n_corr;
+    if (failure != F_OK) st[ST_FAIL] = failure, st[ST_DONE] = 1;
+  }
+}
+
+// Step halving, state update and termination tests (registration.py:443-471) for iteration `it`.
+__global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineArgs a, int it) {
+  __shared__ __align__(16) double sbuf_all[4][32];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 4 + wid;
+  if (c >= a.src.n) return;
+  int* st = a.st_i + 8 * (size_t)c;
+  if (st[ST_DONE]) return;
+  double* sbuf = sbuf_all[wid];
+  const GicpCfgDev cfg = a.cfg;
+  const long long plane = a.plane;
+  const double* wb = a.w_buf + a.src.offset[c];
+  const int nc = st[ST_NCOMPACT];
+  double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
+  double r[9], t[3], xi[6];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) r[q] = pose[q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) xi[q] = pose[12 + q];
+  const double f0 = pose[18];
+  __syncwarp();
+  double scale = 1.0, f_try = 0.0;
+  double r_try[9], t_try[3];
+  bool accepted = false;
+  for (int tr = 0; tr < 9; ++tr) {
+    double rs[9];
+    so3_exp_fast(scale * xi[0], scale * xi[1], scale * xi[2], rs);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        r_try[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
+      t_try[i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
     }
+    f_try = gicp_objective(wb, plane, nc, r_try, t_try, lane, sbuf);
+    if (isfinite(f_try) && f_try <= f0) {
+      accepted = true;
+      break;
+    }
+    scale *= 0.5;
+  }
+  int failure = F_OK, conv = 0;
+  bool done = false;
+  if (!accepted) {
+    failure = F_NO_DECREASE, done = true;
+  } else {
+    renorm_rotation(r_try, r);
+    t[0] = t_try[0], t[1] = t_try[1], t[2] = t_try[2];
+    if (a.out_trace && lane == 0) {
+      double* trace = a.out_trace + 2 * (size_t)cfg.max_iter * c;
+      trace[2 * (it - 1)] = f0, trace[2 * (it - 1) + 1] = f_try;
+    }
+    const double step_t2 = scale * scale * (xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+    const double step_r2 = scale * scale * (xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+    if (step_t2 < cfg.tol_t2 && step_r2 < cfg.tol_r2)
+      conv = 1, done = true;
+    else if (it >= 5 && f0 > 0.0 && (f0 - f_try) <= 1e-4 * f0)
+      done = true;
+    if (lane < 9) pose[lane] = r[lane];
+    if (lane < 3) pose[9 + lane] = t[lane];
+  }
+  if (lane == 0) {
     if (failure != F_OK) st[ST_FAIL] = failure;
     if (failure == F_OK) st[ST_NTRACE] = it;  // an accepted step was recorded
     if (conv) st[ST_CONV] = 1;
@@ -854,7 +941,7 @@ __global__ void __launch_bounds__(128) gicp_finish_kernel(RefineArgs a) {
   const int* st = a.st_i + 8 * (size_t)c;
   const int failure = st[ST_FAIL], iters = st[ST_ITERS], conv = st[ST_CONV];
   const CandView v = cand_view(a, c);
-  const double* pose = a.st_pose + 12 * (size_t)c;
+  const double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
   double r[9], t[3];
 #pragma unroll
   for (int q = 0; q < 9; ++q) r[q] = pose[q];
@@ -932,8 +1019,14 @@ void dump_nn_stats() {
   if (h[0])
     fprintf(stderr, "[nn stats] queries %llu, with prev %.3f, found %.3f; per query: sb tests %.2f, blk tests %.2f, leaves %.2f, leaf pts %.2f\n",
             h[0], (double)h[1] / h[0], (double)h[5] / h[0], (double)h[2] / h[0], (double)h[3] / h[0], (double)h[6] / h[0], (double)h[4] / h[0]);
+  cudaMemcpyFromSymbol(h, g_nn_rhist, sizeof h);
+  fprintf(stderr, "[nn R hist] <0.5 %llu <1.5 %llu <2.5 %llu <3.5 %llu <5.5 %llu <8.5 %llu >=8.5 %llu notfound %llu\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+  cudaMemcpyFromSymbol(h, g_nn_mhist, sizeof h);
+  fprintf(stderr, "[nn motion mm] <.03 %llu <.1 %llu <.3 %llu <1 %llu <3 %llu <10 %llu >=10 %llu\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
   memset(h, 0, sizeof h);
+  cudaMemcpyToSymbol(g_nn_mhist, h, sizeof h);
   cudaMemcpyToSymbol(g_nn_stats, h, sizeof h);
+  cudaMemcpyToSymbol(g_nn_rhist, h, sizeof h);
 }
 #endif
 
@@ -942,20 +1035,33 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches) {
   if (launches) *launches = 0;
   if (a.src.n == 0) return cudaSuccess;
   cudaError_t e;
+#ifdef PX_NN_STATS
+  cudaMemcpyToSymbol(g_nn_rayk, &a.cam.ray_k, sizeof(double));
+  {
+    static float* buf = nullptr;
+    static long long cap = 0;
+    if (cap < a.plane) {
+      if (buf) cudaFree(buf);
+      cudaMalloc(&buf, sizeof(float) * 3 * a.plane), cap = a.plane;
+      cudaMemcpyToSymbol(g_nn_prevq, &buf, sizeof(buf));
+    }
+  }
+#endif
   const int b4 = (a.src.n + 3) / 4;
   const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
   gicp_init_kernel<<<b4, 128, smem_init, st>>>(a);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
-  if ((e = cudaFuncSetAttribute(gicp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   cudaFuncSetAttribute(gicp_nn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all of it as L1
   const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
   for (int it = 1; it <= a.cfg.max_iter; ++it) {
     gicp_nn_kernel<<<b4, 128, 0, st>>>(a, it);
-    gicp_step_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
+    gicp_lin_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
+    gicp_halve_kernel<<<b4, 128, 0, st>>>(a, it);
   }
   gicp_finish_kernel<<<b4, 128, 0, st>>>(a);
-  if (launches) *launches = 2 + 2 * std::max(a.cfg.max_iter, 0);
+  if (launches) *launches = 2 + 3 * std::max(a.cfg.max_iter, 0);
 #ifdef PX_NN_STATS
   cudaStreamSynchronize(st);
   dump_nn_stats();

@@ -105,6 +105,8 @@ struct TargetsDev {
   const float* boxes32;       // per node {cx,cy,cz,hx,hy,hz}: fp32 centre / inflated half-extent of the 3-D box
   const int32_t* leaf_start;  // per target bw*bh+1 entries at [box_off + target index]
   const float4* leaf32;       // (sum) points grouped by block: fp32 copy {x,y,z} + local index bits
+  const double* soa;          // 9 planes of `plane` doubles: x, y, z, c00, c01, c02, c11, c12, c22 (covariances are
+  long long plane;            //   bit-symmetric by construction) -- coalesced / coherent-gather copy for the step kernel
 };
 
 struct CovArgs {  // covariances of a list of clouds (targets), thread per point
@@ -122,6 +124,8 @@ struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   double ray_k;
 };
 cudaError_t launch_cov(const CovArgs& a, long long total_points, cudaStream_t st);
+// (n,3) points + (n,9) covariances -> 9 planes of n doubles (TargetsDev::soa)
+cudaError_t launch_soa(const double* pts, const double* cov, double* soa, long long n, cudaStream_t st);
 
 struct RefineArgs {
   CloudsDev src;
@@ -130,12 +134,13 @@ struct RefineArgs {
   const double* init_T;       // (n,12) or null = identity
   GicpCfgDev cfg;
   Camera cam;
-  // scratch, indexed by the source slot offsets
-  double* src_cov;            // (sum cap,9)
-  double* w_buf;              // (sum cap,9)
+  // scratch, indexed by the source slot offsets; structure-of-arrays with plane stride `plane`
+  long long plane;            // >= sum cap
+  double* src_soa;            // 9 planes: x, y, z, c00, c01, c02, c11, c12, c22 of every source point
+  double* w_buf;              // 15 planes, matched points compacted in index order: W = (Cb + R Ca R^T)^-1 (9), source point (3), target point (3)
   int32_t* corr;              // (sum cap) correspondences of the last linearisation
   int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration
-  double* st_pose;            // (n,12) current iterate [R (9) | t (3)]
+  double* st_pose;            // (n,20) current iterate [R (9) | t (3)], step xi (6), f0, pad
   int32_t* st_i;              // (n,8) per-candidate integer state (px_gicp.cu: ST_*)
   // outputs
   double* out_T;              // (n,12) [orthonormalize(R)|t]

@@ -23,9 +23,9 @@ n = eng.search_upload(plan)
 sc = eng.search_cfg(plan)
 for _ in range(a.steps):
     eng.search_run(sc)
-out = eng.search_download(n)
 import time
 t0 = time.perf_counter()
 eng.search_run(sc)
 eng.sync()
+out = eng.search_download(n)
 print("candidates", n, "stage_ms", out.stage_millis, "wall_ms", (time.perf_counter() - t0) * 1e3)
