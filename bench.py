@@ -130,6 +130,17 @@ def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refi
     d = {"render": float(b_render0.sum()), "rerender": float(b_render1.sum()) if refine else 0.0,
          "refine": float((b_cov + b_iter_sum).sum()) if refine else 0.0, "cost": float(b_cost.sum())}
     d["total"] = sum(d.values())
+    # the refine stage per kernel (B_iter = 104 n_r + 96 n_c + 344 split by which kernel consumes the operand:
+    # nn: source points in, correspondence out, matched target point; lin: source covariances, matched target
+    # point + covariance... the target point is charged to nn, its covariance to lin; halve re-reads operands
+    # the model already charged once, so its algorithmic bytes are 0)
+    nc = ncorr_sum.astype(np.float64)
+    d["kernels"] = {
+        "gicp_init_kernel": float(b_cov.sum()) if refine else 0.0,
+        "gicp_nn_kernel": float((it * 32 * n0 + 24 * nc).sum()) if refine else 0.0,
+        "gicp_lin_kernel": float((it * (72 * n0 + 344) + 72 * nc).sum()) if refine else 0.0,
+        "gicp_halve_kernel": 0.0, "gicp_finish_kernel": 0.0,
+    }
     return d
 
 
@@ -176,6 +187,7 @@ def run_gpu(args):
     # ---- resident-input arm (`value`) ----
     eng.prepare_plan(frame, models, plan)
     n_local = eng.search_upload(plan, idx)
+    eng.set_kernel_timing(True)  # event marks around every refine-stage launch (roofline of the dominant kernel)
     for _ in range(args.warmup):
         eng.search_run(sc)
     out = eng.search_download(n_local)
@@ -183,7 +195,7 @@ def run_gpu(args):
     barrier()
     sampler = ClockSampler(local) if rank == 0 else None
     launches0 = eng.launch_count()
-    step_ms, stage_ms = [], []
+    step_ms, stage_ms, kern_ms = [], [], []
     t_wall0 = time.perf_counter()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed iterations (outside the event pair)
@@ -195,6 +207,7 @@ def run_gpu(args):
         step_ms.append(e0.elapsed_time(e1))
         o = eng.search_download(n_local, full=False)
         stage_ms.append(o.stage_millis)
+        kern_ms.append(eng.kernel_ms())
         reduce_keys(o)
     barrier()
     wall_s = time.perf_counter() - t_wall0
@@ -252,21 +265,38 @@ def run_gpu(args):
     ncs, cap0, cap1 = eng.search_stats(n_local)
     ab = algorithmic_bytes(n_local, models, plan.flat_oid[idx], full, ncs, cap0, cap1, cfg.refine)
     st = {k: float(np.mean([s[k] for s in stage_ms])) for k in stage_ms[0]}
-    dom = max(st, key=st.get)
-    dom_ms = st[dom]
-    achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
-    traffic = None
+    # per kernel: mean over the timed steps of (total ms, launches) per step
+    kern = {k: (float(np.mean([m[k][0] for m in kern_ms])), float(np.mean([m[k][1] for m in kern_ms]))) for k in kern_ms[0]}
+    kern["render_kernel"] = (st["render"] + st["rerender"], 2.0 if cfg.refine else 1.0)
+    kern["cost_kernel"] = (st["cost"], 1.0)
+    kbytes = dict(ab["kernels"])
+    kbytes["render_kernel"] = ab["render"] + ab["rerender"]
+    kbytes["cost_kernel"] = ab["cost"]
+    traffic_db = {}
     tj = ROOT / "profiles" / "traffic.json"
-    kname = {"refine": "gicp_kernel", "render": "render_kernel", "rerender": "render_kernel", "cost": "cost_kernel"}[dom]
     if tj.exists() and args.scale == 1 and world == 1:
-        traffic = json.loads(tj.read_text()).get(args.workload, {}).get(kname, {}).get("dram_bytes_per_launch")
-    roofline = {"bound": "hbm", "kernel": {"refine": "gicp_kernel", "render": "render_kernel", "rerender": "render_kernel",
-                                          "cost": "cost_kernel"}[dom],
-                "achieved": achieved, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic,
-                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of this kernel on this "
-                                "workload (profiles/traffic.json); null when no capture matches",
-                "algorithmic_bytes_per_launch": ab[dom], "kernel_ms": dom_ms,
+        traffic_db = json.loads(tj.read_text()).get(args.workload, {})
+    table = {}
+    for k, (ms, nl) in kern.items():
+        if nl <= 0:
+            continue
+        per_launch_ms, per_launch_b = ms / nl, kbytes.get(k, 0.0) / nl
+        table[k] = {"launches_per_step": nl, "ms_per_step": ms, "ms_per_launch": per_launch_ms,
+                    "algorithmic_bytes_per_launch": per_launch_b,
+                    "achieved_gbs": per_launch_b / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0,
+                    "traffic": traffic_db.get(k, {}).get("dram_bytes_per_launch")}
+    dom = max(table, key=lambda k: table[k]["ms_per_step"])
+    dk = table[dom]
+    refine_gbs = ab["refine"] / (st["refine"] * 1e-3) / 1e9 if st["refine"] > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_gbs"], "peak": hbm_peak, "peak_source": peak_src,
+                "unit": "GB/s", "frac": dk["achieved_gbs"] / hbm_peak, "traffic": dk["traffic"],
+                "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of one launch of this "
+                                "kernel on this workload (profiles/traffic.json); null when no capture matches",
+                "algorithmic_bytes_per_launch": dk["algorithmic_bytes_per_launch"], "kernel_ms": dk["ms_per_launch"],
+                "launches_per_step": dk["launches_per_step"],
+                "timing": "CUDA events recorded on the launch stream around every launch of the GICP stage inside the timed steps",
+                "kernels": table,
+                "refine_stage_achieved": refine_gbs, "refine_stage_frac": refine_gbs / hbm_peak,
                 "whole_step_achieved": ab["total"] / (ms_per_step * 1e-3) / 1e9,
                 "whole_step_frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
                 "bytes_per_candidate": ab["total"] / max(n_local, 1)}

@@ -96,6 +96,10 @@ struct px_ctx {
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
   double stage_ms[4] = {0, 0, 0, 0};
+  bool kernel_timing = false;           // px_ctx_set_kernel_timing
+  std::vector<cudaEvent_t> marks;       // per-launch event marks of the refine stage
+  double kernel_ms[5] = {0, 0, 0, 0, 0};  // gicp init, nn, lin, halve, finish (last px_search_run)
+  int64_t kernel_n[5] = {0, 0, 0, 0, 0};
   int chunks = 0;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
@@ -339,6 +343,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   ctx->clouds.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t e : ctx->marks) cudaEventDestroy(e);
   if (ctx->total_host) cudaFreeHost(ctx->total_host);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -1047,6 +1052,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   CU(cudaMemcpyAsync(ctx->r_nfirst.as<int32_t>() + lo, ctx->clouds.count.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (timed) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
   const double* cost_pose = pose_in;
+  size_t refine_marks = 0;
   if (cfg->refine) {
     if (int r = ensure_refine_scratch(ctx, total, n)) return r;
     RefineArgs a{};
@@ -1067,8 +1073,15 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     memcpy(a.w2c, cfg->world_to_cam, sizeof a.w2c);
     a.c2w_vec_order = cfg->c2w_vec_order, a.w2c_vec_order = cfg->w2c_vec_order, a.fixed_z = cfg->fixed_z;
     int nl = 0;
-    CU(launch_refine(a, ctx->stream, &nl));
+    const size_t n_marks = ctx->kernel_timing ? 3 + 3 * (size_t)std::max(cfg->gicp.max_iterations, 0) : 0;
+    while (ctx->marks.size() < n_marks) {
+      cudaEvent_t e = nullptr;
+      CU(cudaEventCreate(&e));
+      ctx->marks.push_back(e);
+    }
+    CU(launch_refine(a, ctx->stream, &nl, n_marks ? ctx->marks.data() : nullptr));
     ctx->launches += nl;
+    refine_marks = n_marks;
     if (timed) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     if (int r = size_clouds(ctx, ctx->clouds, slot, pose_ref, n, &total)) return r;
     if (int r = render_clouds(ctx, ctx->clouds, slot, pose_ref, n, cfg->occluder_marking, cfg->delta)) return r;
@@ -1090,6 +1103,12 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   for (int i = 0; i < 4; ++i) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) ctx->stage_ms[i] += ms;
+  }
+  for (size_t k = 0; k + 1 < refine_marks; ++k) {  // init, (nn, lin, halve) x iterations, finish
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->marks[k], ctx->marks[k + 1]) != cudaSuccess) continue;
+    const int cls = k == 0 ? 0 : (k + 2 == refine_marks ? 4 : 1 + (int)((k - 1) % 3));
+    ctx->kernel_ms[cls] += ms, ctx->kernel_n[cls] += 1;
   }
   ctx->chunks += 1;
   return 0;
@@ -1126,6 +1145,7 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
     CU(cudaStreamSynchronize(ctx->stream));
   }
   for (double& m : ctx->stage_ms) m = 0.0;
+  for (int i = 0; i < 5; ++i) ctx->kernel_ms[i] = 0.0, ctx->kernel_n[i] = 0;
   if (n == 0) return 0;
   ctx->chunks = 0;
   if (int r = search_range(ctx, cfg, 0, n)) return r;
@@ -1149,6 +1169,21 @@ int px_search_download(px_ctx* ctx, double* refined, double* reg_T, int32_t* ite
   CU(cudaStreamSynchronize(ctx->stream));
   if (stage_ms)
     for (int i = 0; i < 4; ++i) stage_ms[i] = ctx->stage_ms[i];
+  return 0;
+}
+
+int px_ctx_set_kernel_timing(px_ctx* ctx, int32_t on) {
+  if (!ctx) return PX_E_ARG;
+  ctx->kernel_timing = on != 0;
+  return 0;
+}
+
+int px_search_kernel_ms(px_ctx* ctx, double ms[5], int64_t launches[5]) {
+  if (!ctx) return PX_E_ARG;
+  for (int i = 0; i < 5; ++i) {
+    if (ms) ms[i] = ctx->kernel_ms[i];
+    if (launches) launches[i] = ctx->kernel_n[i];
+  }
   return 0;
 }
 

@@ -1093,7 +1093,9 @@ void dump_nn_stats() {
 #endif
 
 // Returns the number of kernels launched through *launches.
-cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches) {
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, cudaEvent_t* marks) {
+  int mk = 0;
+#define PX_MARK() do { if (marks) cudaEventRecord(marks[mk++], st); } while (0)
   if (launches) *launches = 0;
   if (a.src.n == 0) return cudaSuccess;
   cudaError_t e;
@@ -1112,17 +1114,24 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches) {
   const int b4 = (a.src.n + 3) / 4;
   const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
+  PX_MARK();
   gicp_init_kernel<<<b4, 128, smem_init, st>>>(a);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   cudaFuncSetAttribute(gicp_nn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all of it as L1
   const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
   for (int it = 1; it <= a.cfg.max_iter; ++it) {
+    PX_MARK();
     gicp_nn_kernel<<<b4, 128, 0, st>>>(a, it);
+    PX_MARK();
     gicp_lin_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
+    PX_MARK();
     gicp_halve_kernel<<<b4, 128, 0, st>>>(a, it);
   }
+  PX_MARK();
   gicp_finish_kernel<<<b4, 128, 0, st>>>(a);
+  PX_MARK();
+#undef PX_MARK
   if (launches) *launches = 2 + 3 * std::max(a.cfg.max_iter, 0);
 #ifdef PX_NN_STATS
   cudaStreamSynchronize(st);

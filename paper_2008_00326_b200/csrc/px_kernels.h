@@ -158,7 +158,9 @@ struct RefineArgs {
   int c2w_vec_order, w2c_vec_order;
   double fixed_z;
 };
-cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches);
+// Launch order: init, (nn, lin, halve) x max_iter, finish.  `marks` (nullable) receives one event
+// before every launch and one after the last: 3 + 3 * max_iter events.
+cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, cudaEvent_t* marks = nullptr);
 
 struct CostArgs {
   CloudsDev ren;

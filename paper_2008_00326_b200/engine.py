@@ -349,6 +349,17 @@ class Engine:
         N.check(self.ctx, rc, "px_search_stats")
         return nc, c0, c1
 
+    KERNELS = ("gicp_init_kernel", "gicp_nn_kernel", "gicp_lin_kernel", "gicp_halve_kernel", "gicp_finish_kernel")
+
+    def set_kernel_timing(self, on: bool):
+        N.check(self.ctx, self.lib.px_ctx_set_kernel_timing(self.ctx, int(on)), "px_ctx_set_kernel_timing")
+
+    def kernel_ms(self):
+        """{kernel: (total ms, launches)} of the refine stage of the last search_run."""
+        ms, nl = np.zeros(5, dtype=np.float64), np.zeros(5, dtype=np.int64)
+        N.check(self.ctx, self.lib.px_search_kernel_ms(self.ctx, N.ptr(ms, N.f64p), N.ptr(nl, N.i64p)), "px_search_kernel_ms")
+        return {k: (float(m), int(c)) for k, m, c in zip(self.KERNELS, ms, nl)}
+
     def prepare_plan(self, frame, models, plan):
         self.upload_scene(frame, plan.cfg.stride, plan.observed, plan.obs_labels)
         self.upload_models({oid: models[oid] for oid in plan.active})
