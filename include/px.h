@@ -129,6 +129,19 @@ int px_covariances(px_ctx* ctx, const double* points, int64_t n, int32_t k, doub
  * identical either way. */
 int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, const double* points,
                       const int64_t* obs_index /* nullable */, const px_gicp_cfg* cfg);
+/* GICP targets cropped from the uploaded (organised) observed cloud ON THE DEVICE -- replaces
+ * search._build_targets / _capsule_crop (search.py:393-426, :205-214).  3-DoF: target t is
+ * { p : (px-x)^2 + (py-y)^2 + max(z_lo-pz, pz-z_hi, 0)^2 <= radius^2 } over the world-frame observed
+ * points p = cam_to_world o observed, params = (n,5) rows {x, y, z_lo, z_hi, radius}; 6-DoF: target t
+ * is the sub-cloud labelled object_ids[t].  Points keep ascending observed index (np.nonzero order).
+ * Covariances and the search structures are built as in px_targets_upload. */
+int px_targets_build_capsules(px_ctx* ctx, int32_t n_targets, const double* params, const double cam_to_world[12],
+                              const px_gicp_cfg* cfg);
+int px_targets_build_labels(px_ctx* ctx, int32_t n_targets, const int32_t* object_ids, const px_gicp_cfg* cfg);
+/* Sizes and contents of the resident targets: offsets (n_targets+1), points (total,3) and, for
+ * device-built targets, the observed index of every point (any pointer may be NULL). */
+int px_targets_info(px_ctx* ctx, int32_t* n_targets, int64_t* total_points);
+int px_targets_download(px_ctx* ctx, int64_t* offsets, double* points, int32_t* obs_index);
 int px_targets_covariances(px_ctx* ctx, double* cov_out); /* (offsets[n],9), for tests */
 /* m2m_gicp: one source cloud per entry, target_idx into the uploaded targets,
  * init_T (n,12) or NULL = identity.  Outputs (any may be NULL): out_T (n,12)

@@ -69,7 +69,7 @@ struct px_ctx {
   bool have_scene = false, organised = false;
   Camera cam{};
   int64_t n_obs = 0;
-  DevBuf depth, valid, labels, obs_pts, obs_lab, obs_labels, gx, gy, gz, gidx;
+  DevBuf depth, valid, labels, obs_pts, obs_lab, obs_labels, obs_cell, gx, gy, gz, gidx;
   std::vector<int32_t> h_obs_labels, h_obs_src;
   // models
   std::vector<ModelHost*> models;
@@ -82,7 +82,8 @@ struct px_ctx {
   long long tgt_total = 0;
   int tgt_k = 0;
   double tgt_gate = 0.0;
-  DevBuf tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
+  DevBuf tgt_obs, tgt_world, tgt_sizes, tgt_scans, tgt_params,
+         tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
   bool tgt_organised = false;
   // resident candidates
   int64_t n_cand = 0;
@@ -335,6 +336,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
+                    &ctx->obs_cell, &ctx->tgt_obs, &ctx->tgt_world, &ctx->tgt_sizes, &ctx->tgt_scans, &ctx->tgt_params,
                     &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
@@ -422,7 +424,11 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
     gi[(size_t)g] = (int32_t)i;
   }
   ctx->organised = org;
+  std::vector<int32_t> cell((size_t)std::max<int64_t>(n_obs, 1), 0);
   if (org) {
+    for (int64_t i = 0; i < n_obs; ++i)
+      cell[(size_t)i] = (obs_src_px[2 * i + 1] / stride) * c.GW + obs_src_px[2 * i] / stride;
+    if (int r = h2d(ctx, ctx->obs_cell, cell.data(), (size_t)n_obs * 4)) return r;
     if (int r = h2d(ctx, ctx->gx, gx.data(), ng * 8)) return r;
     if (int r = h2d(ctx, ctx->gy, gy.data(), ng * 8)) return r;
     if (int r = h2d(ctx, ctx->gz, gz.data(), ng * 8)) return r;
@@ -840,6 +846,116 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     ctx->launches += 2;
   }
   CU(cudaStreamSynchronize(ctx->stream));  // host staging vectors are stack-owned
+  return 0;
+}
+
+// Common tail of the device-side target builders: sizes -> scans -> allocation -> fill -> covariances.
+static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* cfg) {
+  const int n = a.n_targets;
+  const int k = cfg->k_covariance;
+  if (k < 4 || k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k_covariance out of range [4,32]");
+  if (!(cfg->max_correspondence_distance > 0.0)) return fail(ctx, PX_E_ARG, "max_correspondence_distance must be positive");
+  if (!ctx->have_scene || !ctx->organised) return fail(ctx, PX_E_ARG, "targets can only be cropped from an organised scene cloud");
+  const size_t n1 = (size_t)std::max(n, 1);
+  CU(ctx->tgt_sizes.ensure(3 * n1 * 8));
+  CU(ctx->tgt_scans.ensure(2 * (n1 + 1) * 8));
+  CU(ctx->tgt_off.ensure((n1 + 1) * 8));
+  CU(ctx->tgt_org.ensure(n1 * sizeof(TgtOrg)));
+  CU(ctx->tgt_world.ensure((size_t)std::max<int64_t>(ctx->n_obs, 1) * 24));
+  a.obs_pts = ctx->obs_pts.as<double>(), a.obs_labels = ctx->obs_labels.as<int32_t>();
+  a.obs_cell = ctx->obs_cell.as<int32_t>(), a.n_obs = ctx->n_obs, a.GW = ctx->cam.GW;
+  a.world = ctx->tgt_world.as<double>();
+  a.cnt = ctx->tgt_sizes.as<long long>(), a.cells = a.cnt + n1, a.nodes = a.cells + n1;
+  long long* off = ctx->tgt_off.as<long long>();
+  long long* coff = ctx->tgt_scans.as<long long>();
+  long long* noff = coff + n1 + 1;
+  a.offset = off, a.cells_off = coff, a.nodes_off = noff;
+  a.org = ctx->tgt_org.as<TgtOrg>();
+  long long totals[3] = {0, 0, 0};
+  if (n) {
+    CU(launch_tgt_world(a, ctx->stream));
+    CU(launch_tgt_count(a, ctx->stream));
+    CU(launch_scan(a.cnt, off, off + n, n, ctx->stream));
+    CU(launch_scan(a.cells, coff, coff + n, n, ctx->stream));
+    CU(launch_scan(a.nodes, noff, noff + n, n, ctx->stream));
+    ctx->launches += 5;
+    CU(cudaMemcpyAsync(&totals[0], off + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&totals[1], coff + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&totals[2], noff + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  } else {
+    CU(cudaMemsetAsync(off, 0, 8, ctx->stream));
+  }
+  const long long total = totals[0];
+  const size_t tot1 = (size_t)std::max<long long>(total, 1);
+  CU(ctx->tgt_obs.ensure(tot1 * 4));
+  CU(ctx->tgt_pts.ensure(tot1 * 24));
+  CU(ctx->tgt_pix.ensure(tot1 * 4));
+  CU(ctx->tgt_map.ensure((size_t)std::max<long long>(totals[1], 1) * 4));
+  CU(ctx->tgt_boxes.ensure((size_t)std::max<long long>(totals[2], 1) * 24));
+  CU(ctx->tgt_lstart.ensure((size_t)(totals[2] + n + 1) * 4));
+  CU(ctx->tgt_lpts.ensure(tot1 * 16));
+  CU(ctx->tgt_cov.ensure(tot1 * 72));
+  CU(ctx->tgt_soa.ensure(tot1 * 72));
+  a.tgt_obs = ctx->tgt_obs.as<int32_t>(), a.tgt_pts = ctx->tgt_pts.as<double>(), a.tpix = ctx->tgt_pix.as<int32_t>();
+  a.tmap = ctx->tgt_map.as<int32_t>(), a.boxes32 = ctx->tgt_boxes.as<float>();
+  a.leaf_start = ctx->tgt_lstart.as<int32_t>(), a.leaf32 = ctx->tgt_lpts.as<float4>();
+  ctx->tgt_organised = true;
+  ctx->n_targets = n, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = cfg->max_correspondence_distance;
+  if (n) {
+    CU(cudaMemsetAsync(a.tmap, 0xff, (size_t)std::max<long long>(totals[1], 1) * 4, ctx->stream));
+    CU(launch_tgt_fill(a, ctx->stream));
+    CovArgs c{};
+    c.n_clouds = n, c.offset = off, c.count = nullptr;
+    c.points = a.tgt_pts, c.cov = ctx->tgt_cov.as<double>(), c.k = k, c.eps = cfg->epsilon;
+    c.org = a.org, c.tmap = a.tmap, c.tpix = a.tpix, c.ray_k = ctx->cam.ray_k;
+    CU(launch_cov(c, total, ctx->stream));
+    CU(launch_soa(a.tgt_pts, ctx->tgt_cov.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
+    ctx->launches += 5;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int px_targets_build_capsules(px_ctx* ctx, int32_t n_targets, const double* params, const double cam_to_world[12],
+                              const px_gicp_cfg* cfg) {
+  if (!ctx || !cfg || n_targets < 0 || (n_targets && (!params || !cam_to_world)))
+    return fail(ctx, PX_E_ARG, "px_targets_build_capsules: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  for (long long i = 0; i < 5LL * n_targets; ++i)
+    if (!std::isfinite(params[i])) return fail(ctx, PX_E_ARG, "non-finite capsule parameter");
+  if (int r = h2d(ctx, ctx->tgt_params, params, (size_t)n_targets * 40)) return r;
+  TgtBuildArgs a{};
+  a.n_targets = n_targets, a.mode = 0, a.params = ctx->tgt_params.as<double>();
+  if (n_targets) memcpy(a.c2w, cam_to_world, sizeof a.c2w);
+  return build_targets_device(ctx, a, cfg);
+}
+
+int px_targets_build_labels(px_ctx* ctx, int32_t n_targets, const int32_t* object_ids, const px_gicp_cfg* cfg) {
+  if (!ctx || !cfg || n_targets < 0 || (n_targets && !object_ids))
+    return fail(ctx, PX_E_ARG, "px_targets_build_labels: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  if (int r = h2d(ctx, ctx->tgt_params, object_ids, (size_t)n_targets * 4)) return r;
+  TgtBuildArgs a{};
+  a.n_targets = n_targets, a.mode = 1, a.label_ids = ctx->tgt_params.as<int32_t>();
+  return build_targets_device(ctx, a, cfg);
+}
+
+int px_targets_info(px_ctx* ctx, int32_t* n_targets, int64_t* total_points) {
+  if (!ctx) return PX_E_ARG;
+  if (n_targets) *n_targets = ctx->n_targets;
+  if (total_points) *total_points = ctx->tgt_total;
+  return 0;
+}
+
+int px_targets_download(px_ctx* ctx, int64_t* offsets, double* points, int32_t* obs_index) {
+  if (!ctx) return PX_E_ARG;
+  CU(cudaSetDevice(ctx->device));
+  if (int r = d2h(ctx, offsets, ctx->tgt_off.p, ((size_t)ctx->n_targets + 1) * 8)) return r;
+  if (int r = d2h(ctx, points, ctx->tgt_pts.p, (size_t)ctx->tgt_total * 24)) return r;
+  if (obs_index && ctx->tgt_obs.p)
+    if (int r = d2h(ctx, obs_index, ctx->tgt_obs.p, (size_t)ctx->tgt_total * 4)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 

@@ -109,6 +109,42 @@ struct TargetsDev {
   long long plane;            //   bit-symmetric by construction) -- coalesced / coherent-gather copy for the step kernel
 };
 
+// Device-side construction of GICP targets as subsets of the uploaded organised observed cloud
+// (px_targets.cu; search.py:393-426).
+struct TgtBuildArgs {
+  int n_targets;
+  int mode;                   // 0: capsule crops (3-DoF), 1: label sub-clouds (6-DoF)
+  const double* params;       // mode 0: (n,5) cell x, cell y, z_lo, z_hi, radius (world frame)
+  const int32_t* label_ids;   // mode 1: (n) object ids
+  double c2w[12];             // camera -> world (mode 0)
+  // scene
+  const double* obs_pts;      // (n_obs,3) camera frame
+  const int32_t* obs_labels;  // (n_obs)
+  const int32_t* obs_cell;    // (n_obs) stride-grid cell gy*GW+gx of every observed point
+  long long n_obs;
+  int GW;
+  double* world;              // scratch: 3 planes of n_obs (mode 0)
+  // per-target sizes and their exclusive scans
+  long long* cnt;             // (n)
+  long long* cells;           // (n) w*h
+  long long* nodes;           // (n) bw*bh + sw*sh
+  const long long* offset;    // (n+1) scan of cnt      = TargetsDev::offset
+  const long long* cells_off; // (n+1)
+  const long long* nodes_off; // (n+1)
+  // outputs (same layout as px_targets_upload produces on the host)
+  TgtOrg* org;
+  int32_t* tgt_obs;           // (sum) observed index of every target point
+  double* tgt_pts;            // (sum,3)
+  int32_t* tpix;              // (sum) map cell
+  int32_t* tmap;              // (sum cells), -1 on entry
+  float* boxes32;             // (sum nodes,6)
+  int32_t* leaf_start;        // (sum nodes + n)
+  float4* leaf32;             // (sum)
+};
+cudaError_t launch_tgt_world(const TgtBuildArgs& a, cudaStream_t st);
+cudaError_t launch_tgt_count(const TgtBuildArgs& a, cudaStream_t st);
+cudaError_t launch_tgt_fill(const TgtBuildArgs& a, cudaStream_t st);  // offsets -> fill -> tree
+
 struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   int n_clouds;
   const long long* offset;  // (n_clouds+1) or per-cloud offsets with counts

@@ -1,0 +1,228 @@
+// px_targets.cu -- GICP target clouds built on the device.
+//
+// Replaces search._build_targets / _capsule_crop (reference pkg/src/rvpose/search.py:393-426,
+// :205-214): a target is the sub-cloud of the observed cloud inside a capsule around a 3-DoF grid
+// cell (radius 1.5 r + dt, z in [z_lo, z_hi]) or, in 6-DoF, the points labelled with the object.
+// The reference evaluates one numpy mask over all observed points per target; here one CTA per
+// target evaluates the same predicate with the same operation order (fp64, no contraction; the
+// world-frame point is `p @ R.T + t` in the host BLAS order, px_common.cuh) and compacts the
+// survivors in ascending observed index, which is the order np.nonzero returns.  The organised
+// views the nearest-neighbour search needs (pixel map, two-level box hierarchy, per-block leaf
+// arrays, fp32 error bound) are built here as well, with the rules px_targets_upload applies on
+// the host -- tests compare both paths bit for bit.
+#include "px_kernels.h"
+
+namespace px {
+
+__global__ void obs_world_kernel(const double* __restrict__ pts, long long n, TgtBuildArgs a) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x, y, z;
+  apply_pose(a.c2w, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], x, y, z);
+  a.world[i] = x, a.world[n + i] = y, a.world[2 * n + i] = z;
+}
+
+// membership of observed point i in target t
+__device__ __forceinline__ bool tgt_member(const TgtBuildArgs& a, int t, long long i, const double* prm) {
+  if (a.mode == 1) return a.obs_labels[i] == a.label_ids[t];
+  // search.py:205-214: dx^2 + dy^2 + max(z_lo - z, z - z_hi, 0)^2 <= radius^2
+  const double dx = a.world[i] - prm[0], dy = a.world[a.n_obs + i] - prm[1];
+  const double pz = a.world[2 * a.n_obs + i];
+  const double dz = fmax(fmax(prm[2] - pz, pz - prm[3]), 0.0);
+  return dx * dx + dy * dy + dz * dz <= prm[4] * prm[4];
+}
+
+// pass 1: member count and grid bounding box of every target
+__global__ void __launch_bounds__(256) tgt_count_kernel(TgtBuildArgs a) {
+  const int t = blockIdx.x;
+  __shared__ double prm[5];
+  __shared__ int red[4][8];
+  if (a.mode == 0 && threadIdx.x < 5) prm[threadIdx.x] = a.params[5 * (size_t)t + threadIdx.x];
+  __syncthreads();
+  int cnt = 0, x0 = 1 << 30, y0 = 1 << 30, x1 = -1, y1 = -1;
+  for (long long i = threadIdx.x; i < a.n_obs; i += blockDim.x)
+    if (tgt_member(a, t, i, prm)) {
+      const int cell = a.obs_cell[i], gx = cell % a.GW, gy = cell / a.GW;
+      ++cnt, x0 = min(x0, gx), x1 = max(x1, gx), y0 = min(y0, gy), y1 = max(y1, gy);
+    }
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o)), y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+    x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o)), y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[0][w] = cnt, red[1][w] = x0, red[2][w] = y0, red[3][w] = x1 | (y1 << 16);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int xx1 = -1, yy1 = -1;
+    cnt = 0, x0 = 1 << 30, y0 = 1 << 30;
+    for (int q = 0; q < 8; ++q) {
+      cnt += red[0][q], x0 = min(x0, red[1][q]), y0 = min(y0, red[2][q]);
+      if (red[3][q] >= 0) xx1 = max(xx1, red[3][q] & 0xffff), yy1 = max(yy1, red[3][q] >> 16);
+    }
+    TgtOrg o{};
+    if (cnt > 0) o.gx0 = x0, o.gy0 = y0, o.w = xx1 - x0 + 1, o.h = yy1 - y0 + 1;
+    else o.gx0 = o.gy0 = 0, o.w = 1, o.h = 1;
+    o.bw = (o.w + PX_BLK - 1) / PX_BLK, o.bh = (o.h + PX_BLK - 1) / PX_BLK;
+    o.sw = (o.bw + PX_BLK - 1) / PX_BLK, o.sh = (o.bh + PX_BLK - 1) / PX_BLK;
+    a.org[t] = o;
+    a.cnt[t] = cnt;
+    a.cells[t] = (long long)o.w * o.h;
+    a.nodes[t] = (long long)o.bw * o.bh + (long long)o.sw * o.sh;
+  }
+}
+
+__global__ void tgt_offsets_kernel(TgtBuildArgs a) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= a.n_targets) return;
+  a.org[t].map_off = a.cells_off[t];
+  a.org[t].box_off = a.nodes_off[t];
+}
+
+// pass 2: ordered compaction -> obs index, points, map cell of every member; pixel map; error bound
+__global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
+  const int t = blockIdx.x;
+  __shared__ double prm[5];
+  __shared__ int wcnt[8];
+  __shared__ double wmax[8];
+  if (a.mode == 0 && threadIdx.x < 5) prm[threadIdx.x] = a.params[5 * (size_t)t + threadIdx.x];
+  __syncthreads();
+  const TgtOrg o = a.org[t];
+  const long long off = a.offset[t];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int run = 0;
+  double m = 0.0;
+  for (long long base = 0; base < a.n_obs; base += blockDim.x) {
+    const long long i = base + threadIdx.x;
+    const bool in = i < a.n_obs && tgt_member(a, t, i, prm);
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0) wcnt[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, all = 0;
+    for (int q = 0; q < 8; ++q) {
+      before += q < w ? wcnt[q] : 0;
+      all += wcnt[q];
+    }
+    if (in) {
+      const int pos = run + before + __popc(bal & ((1u << lane) - 1u));
+      const double x = a.obs_pts[3 * i], y = a.obs_pts[3 * i + 1], z = a.obs_pts[3 * i + 2];
+      a.tgt_obs[off + pos] = (int32_t)i;
+      a.tgt_pts[3 * (off + pos)] = x, a.tgt_pts[3 * (off + pos) + 1] = y, a.tgt_pts[3 * (off + pos) + 2] = z;
+      const int cell = a.obs_cell[i];
+      const int lc = (cell / a.GW - o.gy0) * o.w + (cell % a.GW - o.gx0);
+      a.tpix[off + pos] = lc;
+      a.tmap[o.map_off + lc] = pos;
+      m = fmax(m, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+    }
+    run += all;
+    __syncthreads();
+  }
+  for (int q = 16; q; q >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, q));
+  if (lane == 0) wmax[w] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < 8; ++q) m = fmax(m, wmax[q]);
+    a.org[t].err = ldexp(1.5 * (2.0 * m + 1.0), -24);  // px_targets_upload: bound on the fp32 pruning errors
+  }
+}
+
+// fp32 pruning copy of a box: centre / half-extent, the half-extent inflated by the centre's rounding
+__device__ __forceinline__ void box32(const double* lo, const double* hi, float* out) {
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    float cf = 0.f, hf = -1e30f;  // empty node: distance overflows to +inf and is always pruned
+    if (lo[d] <= hi[d]) {
+      const double c = 0.5 * (lo[d] + hi[d]);
+      cf = (float)c;
+      const double h = fmax(hi[d] - (double)cf, (double)cf - lo[d]);
+      hf = (float)h;
+      if ((double)hf < h) hf = nextafterf(hf, CUDART_INF_F);
+    }
+    out[d] = cf, out[3 + d] = hf;
+  }
+}
+
+// pass 3: per target, boxes of every block / super-block, leaf start offsets and leaf arrays
+__global__ void __launch_bounds__(256) tgt_tree_kernel(TgtBuildArgs a) {
+  const int t = blockIdx.x;
+  const TgtOrg o = a.org[t];
+  const long long off = a.offset[t];
+  const int32_t* map = a.tmap + o.map_off;
+  const double* P = a.tgt_pts + 3 * off;
+  const int nb = o.bw * o.bh, ns = o.sw * o.sh;
+  float* bb = a.boxes32 + 6 * o.box_off;
+  int32_t* ls = a.leaf_start + o.box_off + t;
+  // boxes (a thread per node scans the node's map cells)
+  for (int q = threadIdx.x; q < nb + ns; q += blockDim.x) {
+    const bool sup = q >= nb;
+    const int e = sup ? q - nb : q, span = sup ? PX_BLK * PX_BLK : PX_BLK;
+    const int nx = sup ? o.sw : o.bw;
+    const int cx0 = (e % nx) * span, cy0 = (e / nx) * span;
+    double lo[3] = {CUDART_INF, CUDART_INF, CUDART_INF}, hi[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};
+    int cnt = 0;
+    for (int y = cy0; y < min(cy0 + span, o.h); ++y)
+      for (int x = cx0; x < min(cx0 + span, o.w); ++x) {
+        const int j = map[y * o.w + x];
+        if (j < 0) continue;
+        ++cnt;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], P[3 * j + d]), hi[d] = fmax(hi[d], P[3 * j + d]);
+      }
+    box32(lo, hi, bb + 6 * q);
+    if (!sup) ls[q + 1] = cnt;  // turned into offsets below
+  }
+  if (threadIdx.x == 0) ls[0] = 0;
+  __syncthreads();
+  // inclusive scan of the per-block counts (chunked over the CTA)
+  __shared__ int part[256];
+  const int per = (nb + 255) / 256;
+  const int lo_ = min(nb, (int)threadIdx.x * per), hi_ = min(nb, lo_ + per);
+  int s = 0;
+  for (int q = lo_; q < hi_; ++q) s += ls[q + 1];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int d = 1; d < 256; d <<= 1) {
+    const int v = (int)threadIdx.x >= d ? part[threadIdx.x - d] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int q = lo_; q < hi_; ++q) {
+    run += ls[q + 1];
+    ls[q + 1] = run;
+  }
+  __syncthreads();
+  // leaf arrays: the block's points in row-major cell order = ascending local index
+  float4* lp = a.leaf32 + off;
+  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
+    const int cx0 = (q % o.bw) * PX_BLK, cy0 = (q / o.bw) * PX_BLK;
+    int k = ls[q];
+    for (int y = cy0; y < min(cy0 + PX_BLK, o.h); ++y)
+      for (int x = cx0; x < min(cx0 + PX_BLK, o.w); ++x) {
+        const int j = map[y * o.w + x];
+        if (j < 0) continue;
+        lp[k++] = make_float4((float)P[3 * j], (float)P[3 * j + 1], (float)P[3 * j + 2], __int_as_float(j));
+      }
+  }
+}
+
+cudaError_t launch_tgt_world(const TgtBuildArgs& a, cudaStream_t st) {
+  if (a.n_obs > 0 && a.mode == 0)
+    obs_world_kernel<<<(unsigned)((a.n_obs + 255) / 256), 256, 0, st>>>(a.obs_pts, a.n_obs, a);
+  return cudaGetLastError();
+}
+cudaError_t launch_tgt_count(const TgtBuildArgs& a, cudaStream_t st) {
+  if (a.n_targets > 0) tgt_count_kernel<<<a.n_targets, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_tgt_fill(const TgtBuildArgs& a, cudaStream_t st) {
+  if (a.n_targets > 0) {
+    tgt_offsets_kernel<<<(a.n_targets + 255) / 256, 256, 0, st>>>(a);
+    tgt_fill_kernel<<<a.n_targets, 256, 0, st>>>(a);
+    tgt_tree_kernel<<<a.n_targets, 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace px

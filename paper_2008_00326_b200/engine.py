@@ -207,6 +207,31 @@ class Engine:
                                         N.ptr(oi, N.i64p), C.byref(g))
         N.check(self.ctx, rc, "px_targets_upload")
 
+    def build_targets(self, plan):
+        """GICP targets cropped from the resident observed cloud on the device
+        (search.py:393-426) from the plan's target specs."""
+        g = self._gicp_cfg(plan.cfg.gicp)
+        if plan.cfg.mode == "3dof":
+            prm = N.f64(plan.target_capsules)
+            c2w = N.f64(plan.c2w)
+            rc = self.lib.px_targets_build_capsules(self.ctx, prm.shape[0], N.ptr(prm, N.f64p), N.ptr(c2w, N.f64p), C.byref(g))
+            N.check(self.ctx, rc, "px_targets_build_capsules")
+        else:
+            ids = N.i32(plan.target_labels)
+            rc = self.lib.px_targets_build_labels(self.ctx, ids.shape[0], N.ptr(ids, N.i32p), C.byref(g))
+            N.check(self.ctx, rc, "px_targets_build_labels")
+
+    def download_targets(self):
+        """(offsets, points, obs_index) of the resident targets."""
+        n, tot = C.c_int32(0), C.c_int64(0)
+        N.check(self.ctx, self.lib.px_targets_info(self.ctx, C.byref(n), C.byref(tot)), "px_targets_info")
+        off = np.zeros(n.value + 1, dtype=np.int64)
+        pts = np.empty((tot.value, 3))
+        oi = np.zeros(tot.value, dtype=np.int32)
+        rc = self.lib.px_targets_download(self.ctx, N.ptr(off, N.i64p), N.ptr(pts, N.f64p), N.ptr(oi, N.i32p))
+        N.check(self.ctx, rc, "px_targets_download")
+        return off, pts, oi
+
     def target_covariances(self, total) -> np.ndarray:
         out = np.empty((total, 3, 3))
         N.check(self.ctx, self.lib.px_targets_covariances(self.ctx, N.ptr(out, N.f64p)), "px_targets_covariances")
@@ -365,6 +390,8 @@ class Engine:
         self.upload_models({oid: models[oid] for oid in plan.active})
         if plan.cfg.refine and plan.target_offsets is not None:
             self.upload_targets(plan.target_offsets, plan.target_points, plan.cfg.gicp, plan.target_obs_index)
+        elif plan.cfg.refine and plan.target_idx is not None:
+            self.build_targets(plan)
 
     def run_plan(self, frame, models, plan, index=None):
         """Scene/model/target upload + fused search for the plan's candidates."""

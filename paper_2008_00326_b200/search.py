@@ -204,6 +204,8 @@ class SearchPlan:
     target_points: np.ndarray | None = None   # (sum,3) f64
     target_obs_index: np.ndarray | None = None  # (sum,) i64 index into observed
     target_idx: np.ndarray | None = None      # (N,) i32
+    target_capsules: np.ndarray | None = None  # 3-DoF target specs (n_targets,5): x, y, z_lo, z_hi, radius
+    target_labels: np.ndarray | None = None    # 6-DoF target specs (n_targets,) object ids
     c2w: np.ndarray | None = None    # (3,4)
     w2c: np.ndarray | None = None
     c2w_vec_order: int = 0           # 0: rotation C-contiguous, 1: transposed view
@@ -245,8 +247,12 @@ def _vec_order(rotation: np.ndarray) -> int:
     return 0 if rotation.flags.c_contiguous else 1
 
 
-def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = True) -> SearchPlan:
-    """Host part of search.py:217-265 and :393-426."""
+def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = True,
+                materialise_targets: bool = True) -> SearchPlan:
+    """Host part of search.py:217-265 and :393-426.  With `materialise_targets`
+    False only the target SPECS (capsule parameters / label ids) and the
+    candidate -> target map are produced; the device crops the clouds itself
+    (Engine.build_targets)."""
     k = frame.intrinsics
     cam_to_world = RigidTransform(k.camera_pose.rotation, k.camera_pose.translation)
     world_to_cam = cam_to_world.inverse()
@@ -300,26 +306,24 @@ def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = Tr
                       c2w_vec_order=_vec_order(cam_to_world.rotation),
                       w2c_vec_order=_vec_order(world_to_cam.rotation))
     if cfg.refine and build_targets and plan.n:
-        _plan_targets(plan, models, cam_to_world)
+        _plan_targets(plan, models, cam_to_world, materialise_targets)
     return plan
 
 
-def _plan_targets(plan: SearchPlan, models, cam_to_world) -> None:
+def _plan_targets(plan: SearchPlan, models, cam_to_world, materialise: bool = True) -> None:
     """GICP targets (search.py:393-426): the label sub-cloud per object in
     6-DoF; per (object, grid cell) a capsule crop of the observed cloud in
     3-DoF.  Slots are numbered by first appearance in the flat list."""
     cfg, obs = plan.cfg, plan.observed
     n_obs = len(obs)
-    chunks, tidx = [], np.empty(plan.n, dtype=np.int32)
+    tidx = np.empty(plan.n, dtype=np.int32)
     if cfg.mode == "6dof":
-        slot = {}
-        for oid in plan.active:
-            slot[oid] = len(chunks)
-            chunks.append(np.nonzero(plan.obs_labels == oid)[0])
+        slot = {oid: s for s, oid in enumerate(plan.active)}
         for oid in plan.active:
             tidx[plan.flat_oid == oid] = slot[oid]
+        plan.target_labels = np.asarray(plan.active, dtype=np.int32)
     else:
-        obs_world = cam_to_world.apply(obs.points) if n_obs else np.zeros((0, 3))
+        caps = []
         for oid in plan.active:
             sel = np.nonzero(plan.flat_oid == oid)[0]
             ps = plan.proposal_sets[oid]
@@ -330,23 +334,30 @@ def _plan_targets(plan: SearchPlan, models, cam_to_world) -> None:
             cyl = models[oid].inscribed_cylinder
             z_lo, z_hi = cfg.fixed_z + cyl.z_min + 0.005, cfg.fixed_z + cyl.z_max
             radius = 1.5 * cyl.radius + cfg.dt
-            cell_slot = {}
-            for o in order:
-                i = loc[first[o]]
-                x, y = ps.translations[i, 0], ps.translations[i, 1]
-                cell_slot[int(uniq[o])] = len(chunks)
-                chunks.append(np.nonzero(_capsule_mask(obs_world, x, y, z_lo, z_hi, radius))[0])
             lut = np.full(int(uniq.max()) + 1, -1, dtype=np.int32)
-            for c, s in cell_slot.items():
-                lut[c] = s
+            lut[uniq[order]] = len(caps) + np.arange(order.size, dtype=np.int32)
+            rows = loc[first[order]]
+            block = np.empty((order.size, 5))
+            block[:, 0], block[:, 1] = ps.translations[rows, 0], ps.translations[rows, 1]
+            block[:, 2], block[:, 3], block[:, 4] = z_lo, z_hi, radius
+            caps.extend(block)
             tidx[sel] = lut[cells]
+        plan.target_capsules = np.ascontiguousarray(np.array(caps).reshape(-1, 5))
+    plan.target_idx = tidx
+    if not materialise:
+        return
+    if cfg.mode == "6dof":
+        chunks = [np.nonzero(plan.obs_labels == oid)[0] for oid in plan.active]
+    else:
+        obs_world = cam_to_world.apply(obs.points) if n_obs else np.zeros((0, 3))
+        chunks = [np.nonzero(_capsule_mask(obs_world, x, y, z_lo, z_hi, radius))[0]
+                  for x, y, z_lo, z_hi, radius in plan.target_capsules]
     offs = np.zeros(len(chunks) + 1, dtype=np.int64)
     np.cumsum([c.size for c in chunks], out=offs[1:])
     index = np.concatenate(chunks) if chunks else np.zeros(0, np.int64)
     plan.target_offsets = offs
     plan.target_obs_index = index.astype(np.int64)
     plan.target_points = np.ascontiguousarray(obs.points[index]) if n_obs else np.zeros((0, 3))
-    plan.target_idx = tidx
 
 
 # ---------------------------------------------------------------------------
@@ -413,7 +424,7 @@ def estimate_poses(frame, models: dict, cfg: SearchConfig) -> SearchResult:
     from .engine import default_engine
 
     t_start = time.perf_counter()
-    plan = plan_search(frame, models, cfg)
+    plan = plan_search(frame, models, cfg, materialise_targets=False)  # the device crops the GICP targets
     if plan.n == 0:
         out = StageOutputs(np.zeros((0, 3, 4)), np.zeros((0, 3, 4)), np.zeros(0, np.int32),
                            np.zeros(0, np.int32))

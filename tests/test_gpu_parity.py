@@ -334,3 +334,46 @@ def test_organised_targets_equal_generic(engine):
     finally:
         engine.lib.px_clouds_free(engine.ctx, hu)
     assert np.array_equal(Tu, Tg) and np.array_equal(itu, itg)
+
+
+@pytest.mark.parametrize("name", ["c1_box_3dof", "c3_clutter_3dof", "c4_mixed_6dof"])
+def test_device_built_targets_equal_host_plan(engine, name):
+    """search._build_targets on the device (capsule crops in 3-DoF, label sub-clouds in
+    6-DoF): offsets, observed indices, points and covariances are bit-identical to the
+    host plan (which tests/test_oracle_golden.py pins to the reference), and a search
+    that starts from the target SPECS gives the same outputs as one from uploaded clouds."""
+    from paper_2008_00326_b200.search import plan_search
+    d, frame, models, cfg, plan = G.scene(name)
+    spec = plan_search(frame, models, cfg, materialise_targets=False)
+    assert spec.target_points is None and np.array_equal(spec.target_idx, plan.target_idx)
+    engine.upload_scene(frame, cfg.stride, plan.observed, plan.obs_labels)
+    engine.build_targets(spec)
+    off, pts, oi = engine.download_targets()
+    assert np.array_equal(off, plan.target_offsets)
+    assert np.array_equal(oi.astype(np.int64), plan.target_obs_index)
+    assert np.array_equal(pts, plan.target_points)
+    cov_dev = engine.target_covariances(int(off[-1]))
+    engine.upload_targets(plan.target_offsets, plan.target_points, cfg.gicp, plan.target_obs_index)
+    cov_host = engine.target_covariances(int(off[-1]))
+    sizes = np.diff(off)
+    big = np.repeat(sizes > cfg.gicp.k_covariance, sizes)
+    assert np.array_equal(cov_dev[big], cov_host[big])
+    sel = np.arange(0, plan.n, max(1, plan.n // 400))
+    a = engine.run_plan(frame, models, spec, sel)
+    b = engine.run_plan(frame, models, plan, sel)
+    assert np.array_equal(a.refined_cam, b.refined_cam) and np.array_equal(a.iterations, b.iterations)
+    assert np.array_equal(a.j_o, b.j_o) and np.array_equal(a.j_r, b.j_r)
+
+
+def test_device_targets_empty_and_tiny(engine):
+    """Capsules that catch no point, or fewer than k_covariance points, are legal targets
+    (registration.py:504-510: too_few_points keeps the candidate's pose)."""
+    d, frame, models, cfg, plan = G.scene("c1_box_3dof")
+    engine.upload_scene(frame, cfg.stride, plan.observed, plan.obs_labels)
+    caps = np.array([[5.0, 5.0, 0.0, 0.1, 0.05],                  # far outside the scene
+                     list(plan.target_capsules[0][:4]) + [0.004]])  # a few points at most
+    spec = dataclasses.replace(plan, target_capsules=caps, target_points=None, target_offsets=None,
+                               target_obs_index=None)
+    engine.build_targets(spec)
+    off, pts, oi = engine.download_targets()
+    assert off[0] == 0 and off[1] == 0 and off[2] - off[1] <= cfg.gicp.k_covariance
