@@ -796,11 +796,13 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   }
   if (org) {
     // fp32 pruning copies: centre / half-extent with the half-extent inflated by the centre's
-    // rounding (rounded up), and the per-target bound `err` on all fp32 rounding in the tests
-    boxes32.resize(boxes.size());
-    for (size_t q = 0; q < boxes.size() / 6; ++q) {
+    // rounding (rounded up), and the per-target bound `err` on all fp32 rounding in the tests.
+    // Device layout per target (TgtOrg::box_off counts 6-float nodes; 17 per super-block): for every
+    // super-block six planes {cx, cy, cz, hx, hy, hz} x 16 blocks (row-major inside the super-block,
+    // blocks outside the map are empty boxes), then the super-blocks' own {c, h} x 3.
+    auto conv = [](const double* b6, float* c3, float* h3, int stride) {
       for (int d = 0; d < 3; ++d) {
-        const double lo = boxes[6 * q + d], hi = boxes[6 * q + 3 + d];
+        const double lo = b6[d], hi = b6[3 + d];
         float cf = 0.f, hf = -1e30f;  // empty node: distance overflows to +inf and is always pruned
         if (lo <= hi) {
           const double c = 0.5 * (lo + hi);
@@ -809,9 +811,41 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
           hf = (float)h;
           if ((double)hf < h) hf = std::nextafterf(hf, INFINITY);
         }
-        boxes32[6 * q + d] = cf, boxes32[6 * q + 3 + d] = hf;
+        c3[d * stride] = cf, h3[d * stride] = hf;
       }
+    };
+    long long node_total = 0;
+    std::vector<long long> new_off((size_t)n_targets);
+    for (int t = 0; t < n_targets; ++t) {
+      new_off[(size_t)t] = node_total;
+      const long long ns = (long long)orgs[(size_t)t].sw * orgs[(size_t)t].sh;
+      node_total += 17 * ns + (ns & 1);  // even: keeps every target's planes 16-byte aligned
     }
+    boxes32.assign((size_t)node_total * 6, 0.f);
+    std::vector<int32_t> lstart2((size_t)(node_total + n_targets), 0);
+    const double empty6[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int t = 0; t < n_targets; ++t) {
+      TgtOrg& o = orgs[(size_t)t];
+      const double* bbd = boxes.data() + 6 * o.box_off;
+      const double* sbd = bbd + 6 * (long long)o.bw * o.bh;
+      float* out = boxes32.data() + 6 * new_off[(size_t)t];
+      const int ns = o.sw * o.sh;
+      for (int s_ = 0; s_ < ns; ++s_) {
+        float* blk = out + 96 * (size_t)s_;
+        for (int q = 0; q < 16; ++q) {
+          const int by = (s_ / o.sw) * PX_BLK + (q >> 2), bx = (s_ % o.sw) * PX_BLK + (q & 3);
+          const bool in = by < o.bh && bx < o.bw;
+          conv(in ? bbd + 6 * ((long long)by * o.bw + bx) : empty6, blk + q, blk + 48 + q, 16);
+        }
+        float* sbo = out + 96 * (size_t)ns + 6 * (size_t)s_;
+        conv(sbd + 6 * s_, sbo, sbo + 3, 1);
+      }
+      // leaf starts move with the node numbering
+      const int nb_ = o.bw * o.bh;
+      for (int q = 0; q <= nb_; ++q) lstart2[(size_t)(new_off[(size_t)t] + t + q)] = lstart[(size_t)(o.box_off + t + q)];
+      o.box_off = new_off[(size_t)t];
+    }
+    lstart.swap(lstart2);
     for (int t = 0; t < n_targets; ++t) {
       double m = 0.0;
       for (long long i = off[(size_t)t]; i < off[(size_t)t + 1]; ++i)

@@ -362,22 +362,31 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
     const float qxf = (float)qx, qyf = (float)qy, qzf = (float)qz;
     const int32_t* lstart = T.leaf_start + o.box_off + ti;  // (bw*bh + 1) entries per target
     const float4* lp = T.leaf32 + toff;                     // points grouped by block: {x, y, z, index bits}
-    const float* bb = T.boxes32 + 6 * o.box_off;            // blocks {cx,cy,cz,hx,hy,hz}, row-major (bh x bw)
-    const float* sb = bb + 6 * (long long)o.bw * o.bh;      // super-blocks, row-major (sh x sw)
+    // boxes: per super-block six planes {cx,cy,cz,hx,hy,hz} x 16 block slots, then the super-blocks' {c,h}
+    const float* bb = T.boxes32 + 6 * o.box_off;
+    const float* sb = bb + 96 * (long long)o.sw * o.sh;
     for (int sy = 0; sy < o.sh; ++sy)
       for (int sx = 0; sx < o.sw; ++sx) {
         NN_STAT(2, 1);
         if (box_dist2f(sb + 6 * (sy * o.sw + sx), qxf, qyf, qzf) > thr) continue;
-        // phase 1: test the (up to) 16 blocks of this super-block back to back -- independent loads and
-        // arithmetic, no control flow -- and collect the survivors in a bit mask
+        // phase 1: test the 16 block slots of this super-block back to back -- vector loads, independent
+        // arithmetic, no control flow (slots outside the map hold empty boxes) -- survivors into a bit mask
         const int bx0 = sx * PX_BLK, by0 = sy * PX_BLK;
+        const float4* pl = reinterpret_cast<const float4*>(bb + 96 * (sy * o.sw + sx));
         unsigned bmask = 0;
 #pragma unroll
-        for (int q = 0; q < PX_BLK * PX_BLK; ++q) {
-          const int by = by0 + (q >> 2), bx = bx0 + (q & 3);
-          const bool in = by < o.bh && bx < o.bw;
-          const float d = box_dist2f(bb + 6 * (in ? by * o.bw + bx : 0), qxf, qyf, qzf);
-          bmask |= (unsigned)(in && !(d > thr)) << q;
+        for (int g = 0; g < 4; ++g) {
+          const float4 cx = __ldg(pl + g), cy = __ldg(pl + 4 + g), cz = __ldg(pl + 8 + g);
+          const float4 hx = __ldg(pl + 12 + g), hy = __ldg(pl + 16 + g), hz = __ldg(pl + 20 + g);
+#define PX_BT(e, bit)                                                                  \
+  {                                                                                    \
+    const float gx = fmaxf(fabsf(qxf - cx.e) - hx.e, 0.f);                             \
+    const float gy = fmaxf(fabsf(qyf - cy.e) - hy.e, 0.f);                             \
+    const float gz = fmaxf(fabsf(qzf - cz.e) - hz.e, 0.f);                             \
+    bmask |= (unsigned)!(fmaf(gz, gz, fmaf(gy, gy, gx * gx)) > thr) << (4 * g + bit);  \
+  }
+          PX_BT(x, 0) PX_BT(y, 1) PX_BT(z, 2) PX_BT(w, 3)
+#undef PX_BT
         }
         NN_STAT(3, PX_BLK * PX_BLK);
         while (bmask) {

@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(256) tgt_count_kernel(TgtBuildArgs a) {
     a.org[t] = o;
     a.cnt[t] = cnt;
     a.cells[t] = (long long)o.w * o.h;
-    a.nodes[t] = (long long)o.bw * o.bh + (long long)o.sw * o.sh;
+    const long long ns = (long long)o.sw * o.sh;
+    a.nodes[t] = 17 * ns + (ns & 1);  // px_kernels.h: 16 block slots + 1 node per super-block, even count
   }
 }
 
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
 }
 
 // fp32 pruning copy of a box: centre / half-extent, the half-extent inflated by the centre's rounding
-__device__ __forceinline__ void box32(const double* lo, const double* hi, float* out) {
+__device__ __forceinline__ void box32(const double* lo, const double* hi, float* c3, float* h3, int stride) {
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     float cf = 0.f, hf = -1e30f;  // empty node: distance overflows to +inf and is always pruned
@@ -138,7 +139,7 @@ __device__ __forceinline__ void box32(const double* lo, const double* hi, float*
       hf = (float)h;
       if ((double)hf < h) hf = nextafterf(hf, CUDART_INF_F);
     }
-    out[d] = cf, out[3 + d] = hf;
+    c3[d * stride] = cf, h3[d * stride] = hf;
   }
 }
 
@@ -150,26 +151,35 @@ __global__ void __launch_bounds__(256) tgt_tree_kernel(TgtBuildArgs a) {
   const int32_t* map = a.tmap + o.map_off;
   const double* P = a.tgt_pts + 3 * off;
   const int nb = o.bw * o.bh, ns = o.sw * o.sh;
-  float* bb = a.boxes32 + 6 * o.box_off;
+  float* bb = a.boxes32 + 6 * o.box_off;  // per super-block 6 planes x 16 block slots, then the super-block nodes
   int32_t* ls = a.leaf_start + o.box_off + t;
-  // boxes (a thread per node scans the node's map cells)
-  for (int q = threadIdx.x; q < nb + ns; q += blockDim.x) {
-    const bool sup = q >= nb;
-    const int e = sup ? q - nb : q, span = sup ? PX_BLK * PX_BLK : PX_BLK;
-    const int nx = sup ? o.sw : o.bw;
-    const int cx0 = (e % nx) * span, cy0 = (e / nx) * span;
+  // boxes (a thread per block slot / super-block scans the node's map cells)
+  for (int q = threadIdx.x; q < 17 * ns; q += blockDim.x) {
+    const bool sup = q >= 16 * ns;
+    const int s_ = sup ? q - 16 * ns : q >> 4, slot = q & 15;
+    const int span = sup ? PX_BLK * PX_BLK : PX_BLK;
+    const int bx = sup ? s_ % o.sw : (s_ % o.sw) * PX_BLK + (slot & 3), by = sup ? s_ / o.sw : (s_ / o.sw) * PX_BLK + (slot >> 2);
+    const bool in = sup || (bx < o.bw && by < o.bh);
+    const int cx0 = bx * span, cy0 = by * span;
     double lo[3] = {CUDART_INF, CUDART_INF, CUDART_INF}, hi[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};
     int cnt = 0;
-    for (int y = cy0; y < min(cy0 + span, o.h); ++y)
-      for (int x = cx0; x < min(cx0 + span, o.w); ++x) {
-        const int j = map[y * o.w + x];
-        if (j < 0) continue;
-        ++cnt;
+    if (in)
+      for (int y = cy0; y < min(cy0 + span, o.h); ++y)
+        for (int x = cx0; x < min(cx0 + span, o.w); ++x) {
+          const int j = map[y * o.w + x];
+          if (j < 0) continue;
+          ++cnt;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], P[3 * j + d]), hi[d] = fmax(hi[d], P[3 * j + d]);
-      }
-    box32(lo, hi, bb + 6 * q);
-    if (!sup) ls[q + 1] = cnt;  // turned into offsets below
+          for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], P[3 * j + d]), hi[d] = fmax(hi[d], P[3 * j + d]);
+        }
+    if (sup) {
+      float* o6 = bb + 96 * (size_t)ns + 6 * (size_t)s_;
+      box32(lo, hi, o6, o6 + 3, 1);
+    } else {
+      float* blk = bb + 96 * (size_t)s_;
+      box32(lo, hi, blk + slot, blk + 48 + slot, 16);
+      if (in) ls[by * o.bw + bx + 1] = cnt;  // turned into offsets below
+    }
   }
   if (threadIdx.x == 0) ls[0] = 0;
   __syncthreads();
