@@ -10,10 +10,10 @@
 #define PX_TRI_SMEM 64      // meshes up to this many triangles use the per-pixel path
 #define PX_TILE_PIX 4096    // stride-grid pixels per shared-memory z tile (atomic path)
 #ifndef PX_GICP_WARPS
-#define PX_GICP_WARPS 4     // candidates (warps) per CTA in the GICP kernel
+#define PX_GICP_WARPS 2     // candidates (warps) per CTA in the GICP linearise kernel (tuned by sweep)
 #endif
 #ifndef PX_GICP_MINB
-#define PX_GICP_MINB 4      // min resident CTAs per SM requested from ptxas (register budget: 128/thread)
+#define PX_GICP_MINB 8      // min resident CTAs per SM requested from ptxas (register budget: 128/thread)
 #endif
 #define PX_COST_WARPS 4
 #define PX_KCOV_MAX 32
