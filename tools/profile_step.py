@@ -19,6 +19,7 @@ from paper_2008_00326_b200.engine import Engine  # noqa: E402
 frame, models, cfg, plan = bench.build_workload(a.workload, 1, a.scale)
 eng = Engine(0)
 eng.prepare_plan(frame, models, plan)
+eng.set_kernel_timing(True)
 n = eng.search_upload(plan)
 sc = eng.search_cfg(plan)
 for _ in range(a.steps):
@@ -28,4 +29,5 @@ t0 = time.perf_counter()
 eng.search_run(sc)
 eng.sync()
 out = eng.search_download(n)
+print("kernel_ms", {k: round(v[0], 2) for k, v in eng.kernel_ms().items()})
 print("candidates", n, "stage_ms", out.stage_millis, "wall_ms", (time.perf_counter() - t0) * 1e3)
