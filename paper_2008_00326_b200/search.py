@@ -27,7 +27,7 @@ from .cost import CostBreakdown, CostParams
 from .errors import ConfigError, EmptyBatch, NoValidDepth
 from .geometry import RigidTransform, rotation_angle
 from .model import LabeledCloud
-from .proposals import (PoseProposalSet, compose_many, grid_proposals_3dof,
+from .proposals import (PoseProposalSet, compose_grid, compose_many, grid_proposals_3dof,
                         pose_proposals_6dof, rotation_proposals, translation_proposals)
 from .raster import cloud_labels, frame_to_cloud
 from .registration import GicpConfig
@@ -281,7 +281,7 @@ def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = Tr
             continue
         psets[oid] = ps
         if cfg.mode == "3dof":
-            r, t = compose_many(world_to_cam, ps.rotations, ps.translations)
+            r, t = compose_grid(world_to_cam, ps)
         else:
             r, t = ps.rotations, ps.translations
         cams[oid] = np.concatenate([r, t[:, :, None]], axis=2)
