@@ -321,9 +321,32 @@ def unit_fixtures():
     print(f"[units] -> {(OUT / 'units.npz').stat().st_size / 1024:.0f} KiB", flush=True)
 
 
+def tiny_dataset():
+    """A small scene + models directory WRITTEN BY THE REFERENCE (save_scene / save_models,
+    scenegen.py:542-625) and its `estimate` result JSON: pins paper_2008_00326_b200.io and
+    the CLI (tests/test_host_api.py, tests/test_gpu_parity.py)."""
+    import shutil
+    k = sg.make_camera(96, 72)
+    models = {1: sg.mixed_object_suite()[1], 2: sg.mixed_object_suite()[2]}
+    spec = sg.SceneSpec(((1, lift_pose3dof(Pose3Dof(0.05, -0.04, 0.6), 0.0)),
+                         (2, lift_pose3dof(Pose3Dof(-0.08, 0.06, 0.0), 0.0))), (0.42, 0.42), k)
+    frame = disk_roundtrip(sg.generate_scene(spec, models))
+    d = OUT / "dataset_tiny"
+    shutil.rmtree(d, ignore_errors=True)
+    sg.save_scene(d / "scene_0000", frame)
+    sg.save_models(d / "models", models)
+    cfg = rs.SearchConfig(mode="3dof", workspace=(-0.16, 0.16, -0.16, 0.16), stride=1, workers=WORKERS)
+    res = rs.estimate_poses(sg.load_scene(d / "scene_0000"), sg.load_models(d / "models"), cfg)
+    (d / "config.json").write_text(json.dumps({k_: v for k_, v in cfg.to_dict().items() if k_ != "workers"}, indent=2, sort_keys=True))
+    (d / "results_reference.json").write_text(rs.result_to_json(res))
+    print("[dataset_tiny]", sum(f.stat().st_size for f in d.rglob("*") if f.is_file()) // 1024, "KiB", flush=True)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
-    which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c4"}
+    which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c4", "tiny"}
+    if "tiny" in which:
+        tiny_dataset()
     if "units" in which:
         unit_fixtures()
     if "c1" in which:

@@ -377,3 +377,35 @@ def test_device_targets_empty_and_tiny(engine):
     engine.build_targets(spec)
     off, pts, oi = engine.download_targets()
     assert off[0] == 0 and off[1] == 0 and off[2] - off[1] <= cfg.gicp.k_covariance
+
+
+def test_cli_estimate_bench_selftest(engine, tmp_path, capsys):
+    """`estimate` on a dataset written by the reference (tests/golden/dataset_tiny) reproduces the
+    reference's results.json (winner index, integer costs, provenance; pose <= 1e-4), `bench` emits
+    the reference's figure keys, `selftest` passes (cli.py:192-265, 268-335)."""
+    from pathlib import Path
+    from paper_2008_00326_b200.cli import main
+    ds = Path(__file__).resolve().parent / "golden" / "dataset_tiny"
+    out = tmp_path / "out"
+    rc = main(["estimate", "--scene", str(ds / "scene_0000"), "--models", str(ds / "models"), "--out", str(out),
+               "--config", str(ds / "config.json"), "--trace"])
+    assert rc == 0
+    got = json.loads((out / "results.json").read_text())
+    ref = json.loads((ds / "results_reference.json").read_text())
+    assert got["proposals_evaluated"] == ref["proposals_evaluated"]
+    for x, r in zip(got["objects"], ref["objects"]):
+        assert (x["object_id"], x["proposal_index"], x["j_o"], x["j_r"], x["provenance"]) == \
+               (r["object_id"], r["proposal_index"], r["j_o"], r["j_r"], r["provenance"])
+        wt, wr = G.pose_delta(np.array(x["pose"]).reshape(3, 4), np.array(r["pose"]).reshape(3, 4))
+        assert wt <= 1e-4 and wr <= 1e-4
+    assert set(json.loads((out / "timings.json").read_text())) == {"total_millis", "stage_millis", "per_object_millis"}
+    assert len((out / "trace.jsonl").read_text().splitlines()) == ref["proposals_evaluated"]
+    fig = tmp_path / "fig.json"
+    assert main(["bench", "--scene", str(ds / "scene_0000"), "--models", str(ds / "models"), "--config",
+                 str(ds / "config.json"), "--repeat", "2", "--json-out", str(fig)]) == 0
+    f = json.loads(fig.read_text())
+    assert {"proposals", "proposals_per_sec", "total_seconds", "stage_millis", "workers", "rendered_points_max",
+            "observed_points", "knn_full_relation_bytes", "knn_streamed_relation_bytes",
+            "knn_last_relation_bytes"} == set(f) and f["proposals"] == ref["proposals_evaluated"]
+    assert main(["selftest"]) == 0
+    capsys.readouterr()
