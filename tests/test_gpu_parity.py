@@ -409,3 +409,61 @@ def test_cli_estimate_bench_selftest(engine, tmp_path, capsys):
             "knn_last_relation_bytes"} == set(f) and f["proposals"] == ref["proposals_evaluated"]
     assert main(["selftest"]) == 0
     capsys.readouterr()
+
+
+def _full_c3():
+    """BASELINE configs[2] at the size bench.py measures: 58,320 candidates, GICP on."""
+    import bench
+    return bench.build_workload("c3", 1, 1, materialise_targets=False)
+
+
+def test_full_size_determinism_chunking_and_sharding(engine):
+    """Size-independent properties at the benchmark's full size (no oracle run needed):
+    * re-running the same search gives bit-identical outputs (no atomics-order or timing dependence),
+    * forcing the scratch chunking (px_ctx_set_scratch_budget) changes nothing -- candidates are independent,
+    * the per-object argmin of the union of 4 rank shards (dist.shard_index + packed-key MIN, the
+      multi-GPU path) equals the unsharded one, and every shard's per-candidate outputs equal the
+      unsharded rows -- the device analogue of the reference's worker-count determinism test
+      (tests/test_search.py:100-106)."""
+    from paper_2008_00326_b200 import dist as pxd
+    frame, models, cfg, plan = _full_c3()
+    assert plan.n == 58320
+    engine.prepare_plan(frame, models, plan)
+    sc = engine.search_cfg(plan)
+    n = engine.search_upload(plan)
+    engine.search_run(sc)
+    a = engine.search_download(n)
+    engine.search_run(sc)
+    b = engine.search_download(n)
+    for f in ("refined_cam", "reg_T", "j_o", "j_r", "iterations", "flags", "n_rendered"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert a.best_keys == b.best_keys
+    # chunked: 1 GiB of scratch forces several chunks at this size
+    N_ = engine.lib
+    assert N_.px_ctx_set_scratch_budget(engine.ctx, 1 << 30) == 0
+    try:
+        engine.search_run(sc)
+        c = engine.search_download(n)
+    finally:
+        N_.px_ctx_set_scratch_budget(engine.ctx, 8 << 30)
+    for f in ("refined_cam", "j_o", "j_r", "iterations", "flags"):
+        assert np.array_equal(getattr(a, f), getattr(c, f)), f
+    assert a.best_keys == c.best_keys
+    # sharded: 4 ranks' worth of work on this one GPU
+    world = 4
+    keys = []
+    for r in range(world):
+        idx = pxd.shard_index(plan, r, world)
+        m = engine.search_upload(plan, idx)
+        engine.search_run(sc)
+        s = engine.search_download(m)
+        assert np.array_equal(s.refined_cam, a.refined_cam[idx]) and np.array_equal(s.j_o, a.j_o[idx]) \
+            and np.array_equal(s.j_r, a.j_r[idx])
+        keys.append(pxd.keys_from_device(plan, s.best_keys))
+    merged = np.minimum.reduce(keys)
+    assert np.array_equal(merged, pxd.keys_from_device(plan, a.best_keys))
+    # and the winner decoded from the merged keys is the host argmin over all candidates
+    res = assemble_result(plan, a, 0.0)
+    for slot, oid in enumerate(plan.active):
+        e = res.estimate_for(oid)
+        assert (int(merged[slot]) >> 32, int(merged[slot]) & 0xffffffff) == (e.cost.total, e.proposal_index)
