@@ -195,7 +195,7 @@ int size_clouds(px_ctx* ctx, CloudStore& cs, const int32_t* slot_dev, const doub
 }
 
 int render_clouds(px_ctx* ctx, CloudStore& cs, const int32_t* slot_dev, const double* pose_dev, int64_t n,
-                  int occl, double delta_occ) {
+                  int occl, double delta_occ, int skip_lab = 0) {
   size_t tot = (size_t)std::max<long long>(cs.total_cap, 1);
   CU(cs.points.ensure(sizeof(double) * 3 * tot));
   CU(cs.lab.ensure(sizeof(double) * 3 * tot));
@@ -204,7 +204,7 @@ int render_clouds(px_ctx* ctx, CloudStore& cs, const int32_t* slot_dev, const do
   cs.organised = true;
   RenderArgs a = base_render_args(ctx);
   a.model_slot = slot_dev, a.poses = pose_dev, a.n = (int)n;
-  a.occluder_marking = occl, a.delta_occ = delta_occ;
+  a.occluder_marking = occl, a.delta_occ = delta_occ, a.skip_lab = skip_lab;
   a.bbox = cs.bbox.as<int4>(), a.cap = cs.cap.as<long long>(), a.offset = cs.offset.as<long long>();
   a.count = cs.count.as<int32_t>();
   a.points = cs.points.as<double>(), a.lab = cs.lab.as<double>(), a.src_px = cs.src.as<int32_t>();
@@ -241,7 +241,7 @@ int ensure_bitmap(px_ctx* ctx) {
 
 int run_cost(px_ctx* ctx, const CloudStore& cs, const int32_t* slot_dev, const double* cyl_pose_dev, double delta,
              double tau_c, int use_color, int32_t* jo_dev, int32_t* jr_dev, const int32_t* rank_dev,
-             unsigned long long* key_dev) {
+             unsigned long long* key_dev, int lab_is_linear = 0) {
   if (!ctx->organised) return fail(ctx, PX_E_ARG, "scene cloud is not the organised stride-grid cloud");
   if (int r = ensure_bitmap(ctx)) return r;
   CostArgs a{};
@@ -255,7 +255,7 @@ int run_cost(px_ctx* ctx, const CloudStore& cs, const int32_t* slot_dev, const d
   a.obs_lab = ctx->obs_lab.as<double>();
   a.obs_labels = ctx->obs_labels.as<int32_t>();
   a.label_count = ctx->label_count.as<int32_t>();
-  a.delta = delta, a.delta2 = delta * delta, a.tau_c = tau_c, a.use_color = use_color;
+  a.delta = delta, a.delta2 = delta * delta, a.tau_c = tau_c, a.use_color = use_color, a.lab_is_linear = lab_is_linear;
   a.bitmap = ctx->bitmap.as<uint32_t>();
   a.bitmap_words = (ctx->cam.GW * ctx->cam.GH + 31) / 32 + 1;
   a.bitmap_slots = ctx->bitmap_slots;
@@ -1197,7 +1197,8 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     if (int r = search_range(ctx, cfg, lo, mid)) return r;
     return search_range(ctx, cfg, mid, hi);
   }
-  if (int r = render_clouds(ctx, ctx->clouds, slot, pose_in, n, cfg->occluder_marking, cfg->delta)) return r;
+  // with refinement on, the first render only feeds GICP (points); the colours are needed after the re-render
+  if (int r = render_clouds(ctx, ctx->clouds, slot, pose_in, n, cfg->occluder_marking, cfg->delta, cfg->refine ? 1 : 2)) return r;
   CU(cudaMemcpyAsync(ctx->r_cap0.as<long long>() + lo, ctx->clouds.cap.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   CU(cudaMemcpyAsync(ctx->r_nfirst.as<int32_t>() + lo, ctx->clouds.count.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (timed) CU(cudaEventRecord(ctx->ev[1], ctx->stream));
@@ -1234,7 +1235,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     refine_marks = n_marks;
     if (timed) CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     if (int r = size_clouds(ctx, ctx->clouds, slot, pose_ref, n, &total)) return r;
-    if (int r = render_clouds(ctx, ctx->clouds, slot, pose_ref, n, cfg->occluder_marking, cfg->delta)) return r;
+    if (int r = render_clouds(ctx, ctx->clouds, slot, pose_ref, n, cfg->occluder_marking, cfg->delta, 2)) return r;
     cost_pose = pose_ref;
   } else {
     CU(cudaMemcpyAsync(pose_ref, pose_in, (size_t)n * 96, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -1245,7 +1246,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   if (timed) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
   if (int r = run_cost(ctx, ctx->clouds, slot, cfg->mode3dof ? cost_pose : nullptr, cfg->delta, cfg->tau_c, cfg->use_color,
                        ctx->r_jo.as<int32_t>() + lo, ctx->r_jr.as<int32_t>() + lo, ctx->c_rank.as<int32_t>() + lo,
-                       ctx->r_key.as<unsigned long long>()))
+                       ctx->r_key.as<unsigned long long>(), 1))
     return r;
   if (timed) CU(cudaEventRecord(ctx->ev[4], ctx->stream));
   // per-chunk stage times accumulate (a split run is a sequence of such chunks)

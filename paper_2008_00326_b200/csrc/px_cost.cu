@@ -84,7 +84,10 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
     const int j = a.gidx[bg];
     if (a.use_color) {
       const double* ol = a.obs_lab + 3 * (size_t)j;
-      if (!(ciede2000(rl[3 * i], rl[3 * i + 1], rl[3 * i + 2], ol[0], ol[1], ol[2]) <= a.tau_c)) {
+      double L = rl[3 * i], A = rl[3 * i + 1], B = rl[3 * i + 2];
+      if (a.lab_is_linear)  // raster.py:278 evaluated only for the points that reach the colour gate
+        srgb_to_lab(srgb_encode1(L), srgb_encode1(A), srgb_encode1(B), L, A, B);
+      if (!(ciede2000(L, A, B, ol[0], ol[1], ol[2]) <= a.tau_c)) {
         ++color_fail;
         continue;
       }

@@ -38,6 +38,8 @@ struct RenderArgs {
   const double* poses;        // (n,12)
   int n;
   int occluder_marking;
+  int skip_lab;               // 1: leave `lab` unwritten (first render of a refining search: GICP reads points only);
+                              // 2: store the linear-light colour there instead (the cost kernel converts on demand)
   double delta_occ;
   const double* obs_depth;    // (H,W)
   const uint8_t* obs_valid;
@@ -214,6 +216,7 @@ struct CostArgs {
   const int32_t* label_count;  // per model slot: count(obs_labels == oid)
   double delta, delta2, tau_c;
   int use_color;
+  int lab_is_linear;           // ren.lab holds linear-light colours (RenderArgs::skip_lab == 2): convert matched points only
   uint32_t* bitmap;            // scratch: (#warp slots) x bitmap_words, zero on entry and exit
   int bitmap_words;
   int bitmap_slots;            // number of warp slots the bitmap scratch holds (multiple of PX_COST_WARPS)
