@@ -378,6 +378,52 @@ class StageOutputs:
     stage_millis: dict | None = None
 
 
+def _winner_rows(plan: SearchPlan, out: StageOutputs, index=None) -> dict:
+    """Per active object: (packed key, refined pose, applied correction, j_o, j_r) of the best
+    candidate among `out`'s rows (rows = plan candidates `index`, all of them if None):
+    argmin over (total, rank in object), search.py:178-183."""
+    n = out.j_o.shape[0]
+    index = np.arange(plan.n) if index is None else np.asarray(index)
+    total = out.j_o.astype(np.int64) + out.j_r.astype(np.int64)
+    key = (total << 32) | plan.rank_in_object()[index].astype(np.int64)
+    oid = plan.flat_oid[index]
+    rows = {}
+    for o in plan.active:
+        sel = np.nonzero(oid == o)[0]
+        if sel.size:
+            r = int(sel[np.argmin(key[sel])])
+            rows[o] = (int(key[r]), out.refined_cam[r], out.reg_T[r], int(out.j_o[r]), int(out.j_r[r]))
+    assert n == index.shape[0]
+    return rows
+
+
+def _assemble(plan: SearchPlan, winners: dict, stage_millis: dict, t_start: float, max_pts: int) -> SearchResult:
+    """Result records from the per-object winners (search.py:346-377)."""
+    per_stage_total = sum(stage_millis.values())
+    c2w = RigidTransform.from_matrix3x4(plan.c2w)
+    estimates = []
+    for oid in plan.object_ids:
+        if oid in plan.failures or oid not in plan.active or oid not in winners:
+            estimates.append(ObjectEstimate(oid, None, None, None, None, 0.0, 0.0, 0, 0.0,
+                                            failed=True,
+                                            failure=plan.failures.get(oid, "empty_proposal_set")))
+            continue
+        key, refined, reg_T, j_o, j_r = winners[oid]
+        best_local = key & 0xFFFFFFFF
+        n_obj = int(np.count_nonzero(plan.flat_oid == oid))
+        pset = plan.proposal_sets[oid]
+        world = c2w.compose(RigidTransform.from_matrix3x4(refined))
+        delta = RigidTransform.from_matrix3x4(reg_T)
+        share = per_stage_total * (n_obj / max(1, plan.n))
+        estimates.append(ObjectEstimate(
+            oid, world, CostBreakdown(j_o=j_o, j_r=j_r),
+            tuple(int(x) for x in pset.provenance[best_local]), best_local,
+            float(np.linalg.norm(delta.translation)), rotation_angle(delta.rotation),
+            n_obj, share))
+    total_millis = (time.perf_counter() - t_start) * 1e3
+    return SearchResult(tuple(estimates), stage_millis, total_millis, plan.n, max_pts, len(plan.observed))
+
+
 def assemble_result(plan: SearchPlan, out: StageOutputs, t_start: float) -> SearchResult:
     """Per-object argmin and result records (search.py:346-377)."""
     cfg = plan.cfg
@@ -392,37 +438,77 @@ def assemble_result(plan: SearchPlan, out: StageOutputs, t_start: float) -> Sear
                     "object_id": int(plan.flat_oid[j]), "proposal_index": int(plan.flat_local[j]),
                     "j_o": int(out.j_o[j]), "j_r": int(out.j_r[j]), "total": int(total[j]),
                 }, sort_keys=True) + "\n")
-    per_stage_total = sum(stage_millis.values())
-    c2w = RigidTransform.from_matrix3x4(plan.c2w)
-    estimates = []
-    for oid in plan.object_ids:
-        if oid in plan.failures or oid not in plan.active:
-            estimates.append(ObjectEstimate(oid, None, None, None, None, 0.0, 0.0, 0, 0.0,
-                                            failed=True,
-                                            failure=plan.failures.get(oid, "empty_proposal_set")))
-            continue
-        idxs = np.nonzero(plan.flat_oid == oid)[0]
-        best_local = int(np.argmin(total[idxs]))  # first minimum = lowest index
-        j = int(idxs[best_local])
-        pset = plan.proposal_sets[oid]
-        world = c2w.compose(RigidTransform.from_matrix3x4(out.refined_cam[j]))
-        delta = RigidTransform.from_matrix3x4(out.reg_T[j])
-        share = per_stage_total * (len(idxs) / max(1, plan.n))
-        estimates.append(ObjectEstimate(
-            oid, world, CostBreakdown(j_o=int(out.j_o[j]), j_r=int(out.j_r[j])),
-            tuple(int(x) for x in pset.provenance[best_local]), best_local,
-            float(np.linalg.norm(delta.translation)), rotation_angle(delta.rotation),
-            len(idxs), share))
-    total_millis = (time.perf_counter() - t_start) * 1e3
     max_pts = int(out.n_rendered.max()) if out.n_rendered is not None and out.n_rendered.size else 0
-    return SearchResult(tuple(estimates), stage_millis, total_millis, plan.n, max_pts,
-                        len(plan.observed))
+    return _assemble(plan, _winner_rows(plan, out), stage_millis, t_start, max_pts)
+
+
+def estimate_poses_distributed(frame, models: dict, cfg: SearchConfig, runner=None) -> SearchResult:
+    """`estimate_poses` across the ranks of an initialised torch.distributed group (one
+    process per GPU): every rank plans the scene, scores its shard of the candidates
+    (dist.shard_index), and the ranks agree on the per-object winner with ONE
+    all_reduce(MIN) of the packed (cost, pose-id) keys; the owning rank's refined pose
+    travels in a second tiny all_reduce(SUM).  Every rank returns the same SearchResult,
+    identical to the single-process one (the reference's worker-count invariance,
+    tests/test_search.py:100-106).  `runner(frame, models, plan, index) -> StageOutputs`
+    defaults to the device engine; the CPU tests of the host logic inject their own."""
+    import torch
+    import torch.distributed as dist
+
+    from . import dist as pxd
+
+    if cfg.trace_path:
+        raise ConfigError("trace_path is not supported under torch.distributed (per-candidate rows live on their rank)")
+    t_start = time.perf_counter()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    device_run = runner is None
+    if device_run:
+        from .engine import default_engine
+        runner = default_engine().run_plan
+    plan = plan_search(frame, models, cfg, materialise_targets=not device_run)
+    stage_millis = {"render": 0.0, "refine": 0.0, "rerender": 0.0, "cost": 0.0}
+    if plan.n == 0:
+        return _assemble(plan, {}, stage_millis, t_start, 0)
+    idx = pxd.shard_index(plan, rank, world)
+    out = runner(frame, models, plan, idx)
+    if out.stage_millis:
+        stage_millis.update(out.stage_millis)
+    mine = _winner_rows(plan, out, idx)
+    keys = np.array([mine[o][0] if o in mine else pxd.NO_KEY for o in plan.active], dtype=np.int64)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else None
+    best = pxd.allreduce_min(keys, dev)
+    # payload of the winners: only the owning rank contributes non-zeros (keys are unique per candidate)
+    pay = np.zeros((len(plan.active), 27))
+    for s, o in enumerate(plan.active):
+        if o in mine and mine[o][0] == int(best[s]) and best[s] < pxd.NO_KEY:
+            pay[s, :12], pay[s, 12:24] = mine[o][1].reshape(-1), mine[o][2].reshape(-1)
+            pay[s, 24], pay[s, 25], pay[s, 26] = mine[o][3], mine[o][4], 1.0
+    t = torch.from_numpy(pay)
+    t = t.to(dev) if dev is not None else t
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    pay = t.cpu().numpy()
+    mp_t = torch.tensor([float(out.n_rendered.max()) if out.n_rendered is not None and out.n_rendered.size else 0.0]
+                        + [stage_millis[k] for k in ("render", "refine", "rerender", "cost")], dtype=torch.float64)
+    mp_t = mp_t.to(dev) if dev is not None else mp_t
+    dist.all_reduce(mp_t, op=dist.ReduceOp.MAX)  # stage times: slowest rank
+    mp_h = mp_t.cpu().numpy()
+    stage_millis = dict(zip(("render", "refine", "rerender", "cost"), (float(x) for x in mp_h[1:])))
+    winners = {}
+    for s, o in enumerate(plan.active):
+        if pay[s, 26] == 1.0:
+            winners[o] = (int(best[s]), pay[s, :12].reshape(3, 4), pay[s, 12:24].reshape(3, 4), int(pay[s, 24]), int(pay[s, 25]))
+    return _assemble(plan, winners, stage_millis, t_start, int(mp_h[0]))
 
 
 def estimate_poses(frame, models: dict, cfg: SearchConfig) -> SearchResult:
     """Estimate a pose for every detected object (search.py:217-377)."""
     from .engine import default_engine
 
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            return estimate_poses_distributed(frame, models, cfg)
+    except ImportError:
+        pass
     t_start = time.perf_counter()
     plan = plan_search(frame, models, cfg, materialise_targets=False)  # the device crops the GICP targets
     if plan.n == 0:

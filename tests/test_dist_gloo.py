@@ -87,3 +87,46 @@ def test_shard_index_world1_and_keys():
     assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(plan.n))
     assert pxd.unpack_key(pxd.NO_KEY) is None and pxd.unpack_key((7 << 32) | 5) == (7, 5)
     assert np.array_equal(pxd.keys_from_device(plan, {}), np.full(len(plan.active), pxd.NO_KEY))
+
+
+def _worker_api(rank, world, port, name, out_dir):
+    import dataclasses
+
+    import torch.distributed as dist
+
+    import golden_io as G
+    from oracle import oracle as O
+    from paper_2008_00326_b200.search import estimate_poses_distributed, result_to_json
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = G.load(name)
+    frame, models = G.frame_of(d), G.models_of(d)
+    cfg = dataclasses.replace(G.config_of(d), max_proposals=600)
+
+    def runner(frame, models, plan, index):  # the CPU checker stands in for the device engine
+        return O.run_plan(frame, models, plan, n_threads=2, index=index)
+
+    res = estimate_poses_distributed(frame, models, cfg, runner=runner)
+    (Path(out_dir) / f"result_{rank}.json").write_text(result_to_json(res))
+    dist.destroy_process_group()
+
+
+def test_estimate_poses_distributed_equals_single_process(tmp_path):
+    """The public multi-rank entry (refine on, winners' refined poses travelling through the
+    second all_reduce): every rank returns the single-process result JSON byte for byte."""
+    import dataclasses
+
+    import golden_io as G
+    from oracle import oracle as O
+    from paper_2008_00326_b200.search import assemble_result, plan_search, result_to_json
+
+    name, world = "c1_box_3dof", 2
+    mp.spawn(_worker_api, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
+    d = G.load(name)
+    frame, models = G.frame_of(d), G.models_of(d)
+    cfg = dataclasses.replace(G.config_of(d), max_proposals=600)
+    plan = plan_search(frame, models, cfg)
+    single = result_to_json(assemble_result(plan, O.run_plan(frame, models, plan, n_threads=2), 0.0))
+    for r in range(world):
+        assert (tmp_path / f"result_{r}.json").read_text() == single
