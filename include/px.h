@@ -139,7 +139,7 @@ int px_targets_build_capsules(px_ctx* ctx, int32_t n_targets, const double* para
                               const px_gicp_cfg* cfg);
 int px_targets_build_labels(px_ctx* ctx, int32_t n_targets, const int32_t* object_ids, const px_gicp_cfg* cfg);
 /* Sizes and contents of the resident targets: offsets (n_targets+1), points (total,3) and, for
- * device-built targets, the observed index of every point (any pointer may be NULL). */
+ * device-built targets, the observed index of every point (-1 for uploaded targets); any pointer may be NULL. */
 int px_targets_info(px_ctx* ctx, int32_t* n_targets, int64_t* total_points);
 int px_targets_download(px_ctx* ctx, int64_t* offsets, double* points, int32_t* obs_index);
 int px_targets_covariances(px_ctx* ctx, double* cov_out); /* (offsets[n],9), for tests */

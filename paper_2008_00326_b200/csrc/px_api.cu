@@ -85,6 +85,7 @@ struct px_ctx {
   DevBuf tgt_obs, tgt_world, tgt_sizes, tgt_scans, tgt_params,
          tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
   bool tgt_organised = false;
+  bool tgt_obs_valid = false;  // tgt_obs holds the observed indices of the resident targets (device-built)
   // resident candidates
   int64_t n_cand = 0;
   bool have_tidx = false;
@@ -853,7 +854,7 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
       orgs[(size_t)t].err = std::ldexp(1.5 * (2.0 * m + 1.0), -24);
     }
   }
-  ctx->tgt_organised = org;
+  ctx->tgt_organised = org, ctx->tgt_obs_valid = false;
 
   if (int r = h2d(ctx, ctx->tgt_off, off.data(), off.size() * 8)) return r;
   if (int r = h2d(ctx, ctx->tgt_pts, points, (size_t)total * 24)) return r;
@@ -934,7 +935,7 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   a.tgt_obs = ctx->tgt_obs.as<int32_t>(), a.tgt_pts = ctx->tgt_pts.as<double>(), a.tpix = ctx->tgt_pix.as<int32_t>();
   a.tmap = ctx->tgt_map.as<int32_t>(), a.boxes32 = ctx->tgt_boxes.as<float>();
   a.leaf_start = ctx->tgt_lstart.as<int32_t>(), a.leaf32 = ctx->tgt_lpts.as<float4>();
-  ctx->tgt_organised = true;
+  ctx->tgt_organised = true, ctx->tgt_obs_valid = true;
   ctx->n_targets = n, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = cfg->max_correspondence_distance;
   if (n) {
     CU(cudaMemsetAsync(a.tmap, 0xff, (size_t)std::max<long long>(totals[1], 1) * 4, ctx->stream));
@@ -987,8 +988,13 @@ int px_targets_download(px_ctx* ctx, int64_t* offsets, double* points, int32_t* 
   CU(cudaSetDevice(ctx->device));
   if (int r = d2h(ctx, offsets, ctx->tgt_off.p, ((size_t)ctx->n_targets + 1) * 8)) return r;
   if (int r = d2h(ctx, points, ctx->tgt_pts.p, (size_t)ctx->tgt_total * 24)) return r;
-  if (obs_index && ctx->tgt_obs.p)
-    if (int r = d2h(ctx, obs_index, ctx->tgt_obs.p, (size_t)ctx->tgt_total * 4)) return r;
+  if (obs_index) {
+    if (ctx->tgt_obs_valid) {
+      if (int r = d2h(ctx, obs_index, ctx->tgt_obs.p, (size_t)ctx->tgt_total * 4)) return r;
+    } else {
+      for (long long i = 0; i < ctx->tgt_total; ++i) obs_index[i] = -1;  // uploaded targets carry no observed index
+    }
+  }
   CU(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
