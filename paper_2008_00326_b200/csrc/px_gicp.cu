@@ -716,7 +716,11 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
 
   double acc0 = 0.0, acc1 = 0.0;
-  int n_corr = 0;
+  // the running match count lives in shared memory: as a register it gets spilled, and the local-memory reload
+  // queues behind the compaction stores (20 % of this kernel's stall samples)
+  volatile int* n_corr_sm = reinterpret_cast<volatile int*>(hg + 43);
+  if (lane == 0) *n_corr_sm = 0;
+  __syncwarp();
   // software pipeline: a chunk's operands (source point + covariance, gathered target point +
   // covariance) are requested before the ordered sums of the previous chunk, its neighbour
   // indices one chunk earlier still
@@ -825,13 +829,14 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     if (i < n) corr[i] = on ? bj : -1;
     const unsigned onm = __ballot_sync(0xffffffffu, on);
     if (on) {  // ordered compaction for the halving kernel
-      double* o = wb + n_corr + __popc(onm & ((1u << lane) - 1u));
+      double* o = wb + *n_corr_sm + __popc(onm & ((1u << lane) - 1u));
 #pragma unroll
       for (int q = 0; q < 9; ++q) o[q * plane] = w[q];
       o[9 * plane] = ax, o[10 * plane] = ay, o[11 * plane] = az;
       o[12 * plane] = tx, o[13 * plane] = ty, o[14 * plane] = tz;
     }
-    n_corr += __popc(onm);
+    __syncwarp();
+    if (lane == 0) *n_corr_sm += __popc(onm);
     __syncwarp();  // stage writes visible to the summing lanes
     // next chunk's operands: requested last, so that nothing between here and the end of the ordered
     // sums has to wait on a long-latency scoreboard they share
@@ -859,6 +864,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   if (lane < 11) hg[32 + lane] = acc1;
   __syncwarp();
   if (lane == 0) {
+    const int n_corr = *n_corr_sm;
     int failure = F_OK;
     double xi0[6] = {0, 0, 0, 0, 0, 0};
     if (n_corr < 6)
