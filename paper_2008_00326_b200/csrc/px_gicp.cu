@@ -731,9 +731,9 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   for (int q = 0; q < 18; ++q) in[q] = 0.0;
   if (bj_cur >= 0) {
 #pragma unroll
-    for (int q = 0; q < 9; ++q) in[q] = soa[q * plane + lane];
+    for (int q = 0; q < 9; ++q) in[q] = __ldcs(soa + q * plane + lane);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) in[9 + q] = tsoa[q * tplane + bj_cur];
+    for (int q = 0; q < 9; ++q) in[9 + q] = __ldg(tsoa + q * tplane + bj_cur);
   }
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
@@ -831,9 +831,9 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     if (on) {  // ordered compaction for the halving kernel
       double* o = wb + *n_corr_sm + __popc(onm & ((1u << lane) - 1u));
 #pragma unroll
-      for (int q = 0; q < 9; ++q) o[q * plane] = w[q];
-      o[9 * plane] = ax, o[10 * plane] = ay, o[11 * plane] = az;
-      o[12 * plane] = tx, o[13 * plane] = ty, o[14 * plane] = tz;
+      for (int q = 0; q < 9; ++q) __stcs(o + q * plane, w[q]);  // streamed: read once, by the halving kernel
+      __stcs(o + 9 * plane, ax), __stcs(o + 10 * plane, ay), __stcs(o + 11 * plane, az);
+      __stcs(o + 12 * plane, tx), __stcs(o + 13 * plane, ty), __stcs(o + 14 * plane, tz);
     }
     __syncwarp();
     if (lane == 0) *n_corr_sm += __popc(onm);
@@ -844,9 +844,9 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     bj_next = i + 64 < n ? nn[i + 64] : -1;
     if (bj_cur >= 0) {
 #pragma unroll
-      for (int q = 0; q < 9; ++q) in[q] = soa[q * plane + i + 32];
+      for (int q = 0; q < 9; ++q) in[q] = __ldcs(soa + q * plane + i + 32);  // streamed once per iteration
 #pragma unroll
-      for (int q = 0; q < 9; ++q) in[9 + q] = tsoa[q * tplane + bj_cur];
+      for (int q = 0; q < 9; ++q) in[9 + q] = __ldg(tsoa + q * tplane + bj_cur);
     }
     {
       const double* row0 = stage + lane * STAGE_LD;
