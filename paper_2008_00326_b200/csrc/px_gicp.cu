@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
     double cur[15];
     if (lane < nc) {
 #pragma unroll
-      for (int q = 0; q < 15; ++q) cur[q] = wb[q * plane + lane];
+      for (int q = 0; q < 15; ++q) cur[q] = __ldcs(wb + q * plane + lane);
     }
     for (int base = 0; base < nc; base += 32) {
       const int k = base + lane;
@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
       __syncwarp();
       if (k + 32 < nc) {  // next chunk's operands are in flight during the ordered sums
 #pragma unroll
-        for (int q = 0; q < 15; ++q) cur[q] = wb[q * plane + k + 32];
+        for (int q = 0; q < 15; ++q) cur[q] = __ldcs(wb + q * plane + k + 32);
       }
       const double2* s2 = reinterpret_cast<const double2*>(sm_term[wid][my]);
 #pragma unroll
