@@ -81,8 +81,8 @@ struct px_ctx {
   int n_targets = 0;
   long long tgt_total = 0;
   int tgt_k = 0;
-  double tgt_gate = 0.0;
-  DevBuf tgt_obs, tgt_world, tgt_sizes, tgt_scans, tgt_params,
+  double tgt_gate = 0.0, tgt_eps = 0.0;
+  DevBuf tgt_v0, tgt_obs, tgt_world, tgt_sizes, tgt_scans, tgt_params,
          tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
   bool tgt_organised = false;
   bool tgt_obs_valid = false;  // tgt_obs holds the observed indices of the resident targets (device-built)
@@ -337,7 +337,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   }
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
-                    &ctx->obs_cell, &ctx->tgt_obs, &ctx->tgt_world, &ctx->tgt_sizes, &ctx->tgt_scans, &ctx->tgt_params,
+                    &ctx->obs_cell, &ctx->tgt_v0, &ctx->tgt_obs, &ctx->tgt_world, &ctx->tgt_sizes, &ctx->tgt_scans, &ctx->tgt_params,
                     &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
@@ -687,6 +687,7 @@ static TargetsDev targets_dev(px_ctx* ctx) {
   t.leaf32 = ctx->tgt_lpts.as<float4>();
   t.soa = ctx->tgt_soa.as<double>();
   t.plane = std::max<long long>(ctx->tgt_total, 1);
+  t.f = 1.0 - ctx->tgt_eps;
   return t;
 }
 
@@ -868,16 +869,17 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   }
   const size_t tot1 = (size_t)std::max<long long>(total, 1);
   CU(ctx->tgt_cov.ensure(tot1 * 72));
-  ctx->n_targets = n_targets, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = gate;
+  ctx->n_targets = n_targets, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = gate, ctx->tgt_eps = cfg->epsilon;
   if (n_targets) {
     CovArgs a{};
     a.n_clouds = n_targets, a.offset = ctx->tgt_off.as<long long>(), a.count = nullptr;
-    a.points = ctx->tgt_pts.as<double>(), a.cov = ctx->tgt_cov.as<double>(), a.k = k, a.eps = cfg->epsilon;
+    CU(ctx->tgt_v0.ensure(tot1 * 24));
+    a.points = ctx->tgt_pts.as<double>(), a.cov = ctx->tgt_cov.as<double>(), a.v0 = ctx->tgt_v0.as<double>(), a.k = k, a.eps = cfg->epsilon;
     if (org) a.org = ctx->tgt_org.as<TgtOrg>(), a.tmap = ctx->tgt_map.as<int32_t>(), a.tpix = ctx->tgt_pix.as<int32_t>();
     a.ray_k = ctx->cam.ray_k;
     CU(launch_cov(a, total, ctx->stream));
     CU(ctx->tgt_soa.ensure(tot1 * 72));
-    CU(launch_soa(ctx->tgt_pts.as<double>(), ctx->tgt_cov.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
+    CU(launch_soa(ctx->tgt_pts.as<double>(), ctx->tgt_v0.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
     ctx->launches += 2;
   }
   CU(cudaStreamSynchronize(ctx->stream));  // host staging vectors are stack-owned
@@ -931,21 +933,23 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   CU(ctx->tgt_lstart.ensure((size_t)(totals[2] + n + 1) * 4));
   CU(ctx->tgt_lpts.ensure(tot1 * 16));
   CU(ctx->tgt_cov.ensure(tot1 * 72));
+  CU(ctx->tgt_v0.ensure(tot1 * 24));
   CU(ctx->tgt_soa.ensure(tot1 * 72));
   a.tgt_obs = ctx->tgt_obs.as<int32_t>(), a.tgt_pts = ctx->tgt_pts.as<double>(), a.tpix = ctx->tgt_pix.as<int32_t>();
   a.tmap = ctx->tgt_map.as<int32_t>(), a.boxes32 = ctx->tgt_boxes.as<float>();
   a.leaf_start = ctx->tgt_lstart.as<int32_t>(), a.leaf32 = ctx->tgt_lpts.as<float4>();
   ctx->tgt_organised = true, ctx->tgt_obs_valid = true;
   ctx->n_targets = n, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = cfg->max_correspondence_distance;
+  ctx->tgt_eps = cfg->epsilon;
   if (n) {
     CU(cudaMemsetAsync(a.tmap, 0xff, (size_t)std::max<long long>(totals[1], 1) * 4, ctx->stream));
     CU(launch_tgt_fill(a, ctx->stream));
     CovArgs c{};
     c.n_clouds = n, c.offset = off, c.count = nullptr;
-    c.points = a.tgt_pts, c.cov = ctx->tgt_cov.as<double>(), c.k = k, c.eps = cfg->epsilon;
+    c.points = a.tgt_pts, c.cov = ctx->tgt_cov.as<double>(), c.v0 = ctx->tgt_v0.as<double>(), c.k = k, c.eps = cfg->epsilon;
     c.org = a.org, c.tmap = a.tmap, c.tpix = a.tpix, c.ray_k = ctx->cam.ray_k;
     CU(launch_cov(c, total, ctx->stream));
-    CU(launch_soa(a.tgt_pts, ctx->tgt_cov.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
+    CU(launch_soa(a.tgt_pts, ctx->tgt_v0.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
     ctx->launches += 5;
   }
   CU(cudaStreamSynchronize(ctx->stream));

@@ -26,7 +26,16 @@ namespace px {
 
 enum { F_OK = 0, F_TOO_FEW = 1, F_DEGENERATE = 2, F_SINGULAR = 3, F_NO_DECREASE = 4 };
 
-// registration.py:117-216 for point i of a cloud of n points (n > k)
+// registration.py:206-216: C = I - (1 - eps) v0 v0^T, written entry by entry.  The matrix is a pure function
+// of (v0, eps), so the GICP scratch and the target planes keep the 3 doubles of v0 instead of the 6 distinct
+// entries and the linearise kernel re-evaluates these very expressions (same bits, a third less traffic).
+__device__ __forceinline__ void cov_from_normal(double x, double y, double z, double f, double* __restrict__ out) {
+  out[0] = 1.0 - f * x * x, out[1] = -f * x * y, out[2] = -f * x * z;
+  out[3] = out[1], out[4] = 1.0 - f * y * y, out[5] = -f * y * z;
+  out[6] = out[2], out[7] = out[5], out[8] = 1.0 - f * z * z;
+}
+
+// registration.py:117-216 for point i of a cloud of n points (n > k); out = covariance (9) + v0 (3)
 __device__ void cov_point(const double* __restrict__ pts, int n, int i, int k, double eps, double* __restrict__ out) {
   double nd[PX_KCOV_MAX];
   int ni[PX_KCOV_MAX];
@@ -100,10 +109,8 @@ __device__ void cov_point(const double* __restrict__ pts, int n, int i, int k, d
   double dmin = a[0][0], x = vm[0][0], y = vm[1][0], z = vm[2][0];
   if (a[1][1] < dmin) dmin = a[1][1], x = vm[0][1], y = vm[1][1], z = vm[2][1];
   if (a[2][2] < dmin) dmin = a[2][2], x = vm[0][2], y = vm[1][2], z = vm[2][2];
-  const double f = 1.0 - eps;
-  out[0] = 1.0 - f * x * x, out[1] = -f * x * y, out[2] = -f * x * z;
-  out[3] = out[1], out[4] = 1.0 - f * y * y, out[5] = -f * y * z;
-  out[6] = out[2], out[7] = out[5], out[8] = 1.0 - f * z * z;
+  cov_from_normal(x, y, z, 1.0 - eps, out);
+  out[9] = x, out[10] = y, out[11] = z;
 }
 
 // ---------------------------------------------------------------------------
@@ -226,10 +233,8 @@ __device__ __forceinline__ void cov_from_neighbours(const double* __restrict__ p
   double dmin = a[0][0], x = vm[0][0], y = vm[1][0], z = vm[2][0];
   if (a[1][1] < dmin) dmin = a[1][1], x = vm[0][1], y = vm[1][1], z = vm[2][1];
   if (a[2][2] < dmin) dmin = a[2][2], x = vm[0][2], y = vm[1][2], z = vm[2][2];
-  const double f = 1.0 - eps;
-  out[0] = 1.0 - f * x * x, out[1] = -f * x * y, out[2] = -f * x * z;
-  out[3] = out[1], out[4] = 1.0 - f * y * y, out[5] = -f * y * z;
-  out[6] = out[2], out[7] = out[5], out[8] = 1.0 - f * z * z;
+  cov_from_normal(x, y, z, 1.0 - eps, out);
+  out[9] = x, out[10] = y, out[11] = z;
 }
 
 __device__ void cov_point_org(const OrgView& V, int i, int cx, int cy, int k, double eps, double ray_k, double* __restrict__ out) {
@@ -245,6 +250,12 @@ __device__ void cov_point_org_sm(const OrgView& V, int i, int cx, int cy, int k,
   cov_from_neighbours<32>(V.pts, ni, k, eps, out);
 }
 
+__device__ __forceinline__ void store_cov(const CovArgs& a, long long i, const double* cv) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) a.cov[9 * i + q] = cv[q];
+  if (a.v0) a.v0[3 * i] = cv[9], a.v0[3 * i + 1] = cv[10], a.v0[3 * i + 2] = cv[11];
+}
+
 // one CTA per target cloud, threads over its points
 __global__ void __launch_bounds__(128) cov_kernel(CovArgs a) {
   const int c = blockIdx.x;
@@ -257,10 +268,16 @@ __global__ void __launch_bounds__(128) cov_kernel(CovArgs a) {
     OrgView V{a.points + 3 * off, a.tmap + o.map_off, o.w, o.h};
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int cell = a.tpix[off + i];
-      cov_point_org(V, i, cell % o.w, cell / o.w, a.k, a.eps, a.ray_k, a.cov + 9 * (off + i));
+      double cv[12];
+      cov_point_org(V, i, cell % o.w, cell / o.w, a.k, a.eps, a.ray_k, cv);
+      store_cov(a, off + i, cv);
     }
   } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) cov_point(a.points + 3 * off, n, i, a.k, a.eps, a.cov + 9 * (off + i));
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double cv[12];
+      cov_point(a.points + 3 * off, n, i, a.k, a.eps, cv);
+      store_cov(a, off + i, cv);
+    }
   }
 }
 
@@ -270,18 +287,16 @@ cudaError_t launch_cov(const CovArgs& a, long long, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-__global__ void soa_kernel(const double* __restrict__ pts, const double* __restrict__ cov, double* __restrict__ soa, long long n) {
+__global__ void soa_kernel(const double* __restrict__ pts, const double* __restrict__ v0, double* __restrict__ soa, long long n) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double* c = cov + 9 * i;
   soa[i] = pts[3 * i], soa[n + i] = pts[3 * i + 1], soa[2 * n + i] = pts[3 * i + 2];
-  soa[3 * n + i] = c[0], soa[4 * n + i] = c[1], soa[5 * n + i] = c[2];
-  soa[6 * n + i] = c[4], soa[7 * n + i] = c[5], soa[8 * n + i] = c[8];
+  soa[3 * n + i] = v0[3 * i], soa[4 * n + i] = v0[3 * i + 1], soa[5 * n + i] = v0[3 * i + 2];
 }
 
-cudaError_t launch_soa(const double* pts, const double* cov, double* soa, long long n, cudaStream_t st) {
+cudaError_t launch_soa(const double* pts, const double* v0, double* soa, long long n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  soa_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pts, cov, soa, n);
+  soa_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pts, v0, soa, n);
   return cudaGetLastError();
 }
 
@@ -597,8 +612,7 @@ __device__ __forceinline__ CandView cand_view(const RefineArgs& a, int c) {
 // the covariance is bit-symmetric (registration.py:211-216 writes v0 v0^T entry by entry with commuting products)
 __device__ __forceinline__ void store_src_soa(double* soa, long long plane, int i, const double* src, const double* cv) {
   soa[i] = src[3 * i], soa[plane + i] = src[3 * i + 1], soa[2 * plane + i] = src[3 * i + 2];
-  soa[3 * plane + i] = cv[0], soa[4 * plane + i] = cv[1], soa[5 * plane + i] = cv[2];
-  soa[6 * plane + i] = cv[4], soa[7 * plane + i] = cv[5], soa[8 * plane + i] = cv[8];
+  soa[3 * plane + i] = cv[9], soa[4 * plane + i] = cv[10], soa[5 * plane + i] = cv[11];
 }
 
 __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
@@ -609,7 +623,7 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
   const CandView v = cand_view(a, c);
   const GicpCfgDev cfg = a.cfg;
   const double* src = a.src.points + 3 * v.off;
-  double* soa = a.src_soa + v.off;  // planes x, y, z, c00, c01, c02, c11, c12, c22
+  double* soa = a.src_soa + v.off;  // planes x, y, z, v0x, v0y, v0z
   const long long plane = a.plane;
   int* st = a.st_i + 8 * (size_t)c;
   double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
@@ -632,13 +646,13 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
     double* nd = sm + (size_t)wid * (cfg.k_cov * 48) + lane;
     int* ni = reinterpret_cast<int*>(sm + (size_t)wid * (cfg.k_cov * 48) + cfg.k_cov * 32) + lane;
     for (int i = lane; i < v.n; i += 32) {
-      double cv[9];
+      double cv[12];
       cov_point_org_sm(V, i, spx[2 * i] / stp - bb.x, spx[2 * i + 1] / stp - bb.y, cfg.k_cov, cfg.eps, a.cam.ray_k, cv, nd, ni);
       store_src_soa(soa, plane, i, src, cv);
     }
   } else {
     for (int i = lane; i < v.n; i += 32) {
-      double cv[9];
+      double cv[12];
       cov_point(src, v.n, i, cfg.k_cov, cfg.eps, cv);
       store_src_soa(soa, plane, i, src, cv);
     }
@@ -701,12 +715,13 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   double* hg = stage + 43 * STAGE_LD;                  // [43]: H (36), g (6), f0
   const CandView v = cand_view(a, c);
   const int n = v.n;
-  const double* soa = a.src_soa + v.off;  // planes x, y, z, c00, c01, c02, c11, c12, c22
+  const double* soa = a.src_soa + v.off;  // planes x, y, z, v0x, v0y, v0z
   const long long plane = a.plane;
   double* wb = a.w_buf + v.off;           // 15 compact planes
   int32_t* corr = a.corr + v.off;
   const int32_t* nn = a.nn + v.off;
-  const double* tsoa = a.tgt.soa + v.toff;  // same nine planes of the target
+  const double* tsoa = a.tgt.soa + v.toff;  // same six planes of the target
+  const double f_src = 1.0 - a.cfg.eps, f_tgt = a.tgt.f;
   const long long tplane = a.tgt.plane;
   double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
   double r[9], t[3];
@@ -726,14 +741,14 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   // indices one chunk earlier still
   int bj_cur = lane < n ? nn[lane] : -1;
   int bj_next = lane + 32 < n ? nn[lane + 32] : -1;
-  double in[18];  // ax ay az | ca00 ca01 ca02 ca11 ca12 ca22 | tx ty tz | cb00 .. cb22
+  double in[12];  // ax ay az | source v0 | tx ty tz | target v0
 #pragma unroll
-  for (int q = 0; q < 18; ++q) in[q] = 0.0;
+  for (int q = 0; q < 12; ++q) in[q] = 0.0;
   if (bj_cur >= 0) {
 #pragma unroll
-    for (int q = 0; q < 9; ++q) in[q] = __ldcs(soa + q * plane + lane);
+    for (int q = 0; q < 6; ++q) in[q] = __ldcs(soa + q * plane + lane);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) in[9 + q] = __ldg(tsoa + q * tplane + bj_cur);
+    for (int q = 0; q < 6; ++q) in[6 + q] = __ldg(tsoa + q * tplane + bj_cur);
   }
   for (int base = 0; base < n; base += 32) {
     const int i = base + lane;
@@ -743,13 +758,11 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     // never-negative-zero accumulators unchanged -- and all lanes run one uniform staging pass
     double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     double px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0;
-    const double ax = in[0], ay = in[1], az = in[2], tx = in[9], ty = in[10], tz = in[11];
+    const double ax = in[0], ay = in[1], az = in[2], tx = in[6], ty = in[7], tz = in[8];
     if (bj >= 0) {
       double cai[9], cbj[9];
-      cai[0] = in[3], cai[1] = in[4], cai[2] = in[5], cai[4] = in[6], cai[5] = in[7], cai[8] = in[8];
-      cai[3] = cai[1], cai[6] = cai[2], cai[7] = cai[5];
-      cbj[0] = in[12], cbj[1] = in[13], cbj[2] = in[14], cbj[4] = in[15], cbj[5] = in[16], cbj[8] = in[17];
-      cbj[3] = cbj[1], cbj[6] = cbj[2], cbj[7] = cbj[5];
+      cov_from_normal(in[3], in[4], in[5], f_src, cai);
+      cov_from_normal(in[9], in[10], in[11], f_tgt, cbj);
       double rc[9], m[9];
 #pragma unroll
       for (int u = 0; u < 3; ++u)
@@ -844,9 +857,9 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     bj_next = i + 64 < n ? nn[i + 64] : -1;
     if (bj_cur >= 0) {
 #pragma unroll
-      for (int q = 0; q < 9; ++q) in[q] = __ldcs(soa + q * plane + i + 32);  // streamed once per iteration
+      for (int q = 0; q < 6; ++q) in[q] = __ldcs(soa + q * plane + i + 32);  // streamed once per iteration
 #pragma unroll
-      for (int q = 0; q < 9; ++q) in[9 + q] = __ldg(tsoa + q * tplane + bj_cur);
+      for (int q = 0; q < 6; ++q) in[6 + q] = __ldg(tsoa + q * tplane + bj_cur);
     }
     {
       const double* row0 = stage + lane * STAGE_LD;

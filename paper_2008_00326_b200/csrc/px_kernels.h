@@ -107,8 +107,9 @@ struct TargetsDev {
   const float* boxes32;       // per node {cx,cy,cz,hx,hy,hz}: fp32 centre / inflated half-extent of the 3-D box
   const int32_t* leaf_start;  // per target bw*bh+1 entries at [box_off + target index]
   const float4* leaf32;       // (sum) points grouped by block: fp32 copy {x,y,z} + local index bits
-  const double* soa;          // 9 planes of `plane` doubles: x, y, z, c00, c01, c02, c11, c12, c22 (covariances are
-  long long plane;            //   bit-symmetric by construction) -- coalesced / coherent-gather copy for the step kernel
+  const double* soa;          // 6 planes of `plane` doubles: x, y, z and the normal v0 the covariance I - f v0 v0^T is
+  long long plane;            //   made of -- coherent-gather copy for the linearise kernel, which rebuilds the matrix
+  double f;                   // 1 - epsilon the target covariances were built with
 };
 
 // Device-side construction of GICP targets as subsets of the uploaded organised observed cloud
@@ -153,6 +154,7 @@ struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   const int32_t* count;     // nullable: if null, count = offset[i+1]-offset[i]
   const double* points;
   double* cov;              // (sum,9)
+  double* v0;               // (sum,3) nullable: the normal each covariance was made of
   int k;
   double eps;
   // organised targets (nullable): ring search instead of the linear scan
@@ -162,8 +164,8 @@ struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   double ray_k;
 };
 cudaError_t launch_cov(const CovArgs& a, long long total_points, cudaStream_t st);
-// (n,3) points + (n,9) covariances -> 9 planes of n doubles (TargetsDev::soa)
-cudaError_t launch_soa(const double* pts, const double* cov, double* soa, long long n, cudaStream_t st);
+// (n,3) points + (n,3) covariance normals -> 6 planes of n doubles (TargetsDev::soa)
+cudaError_t launch_soa(const double* pts, const double* v0, double* soa, long long n, cudaStream_t st);
 
 struct RefineArgs {
   CloudsDev src;
@@ -174,7 +176,7 @@ struct RefineArgs {
   Camera cam;
   // scratch, indexed by the source slot offsets; structure-of-arrays with plane stride `plane`
   long long plane;            // >= sum cap
-  double* src_soa;            // 9 planes: x, y, z, c00, c01, c02, c11, c12, c22 of every source point
+  double* src_soa;            // 6 planes: x, y, z and the covariance normal v0 of every source point
   double* w_buf;              // 15 planes, matched points compacted in index order: W = (Cb + R Ca R^T)^-1 (9), source point (3), target point (3)
   int32_t* corr;              // (sum cap) correspondences of the last linearisation
   int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration
