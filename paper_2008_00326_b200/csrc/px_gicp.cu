@@ -589,7 +589,7 @@ __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync
 // where the loop counter lives changed.
 
 // per-candidate integer state (RefineArgs::st_i, 8 ints each)
-enum { ST_FAIL = 0, ST_DONE = 1, ST_ITERS = 2, ST_CONV = 3, ST_NTRACE = 4, ST_NCORR = 5, ST_NCOMPACT = 6 };
+enum { ST_FAIL = 0, ST_DONE = 1, ST_ITERS = 2, ST_CONV = 3, ST_NTRACE = 4, ST_NCORR = 5, ST_NCOMPACT = 6, ST_LASTTR = 7 };
 #define ST_POSE_LD 20  // per-candidate double state: R (9), t (3), xi (6), f0, pad
 #ifndef PX_HALVE_MINB
 #define PX_HALVE_MINB 6
@@ -902,13 +902,17 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
 // run side by side in different lanes), and the first acceptable one in trial order is kept --
 // the same decision from the same f values.  Measured trial histogram on C3: 54 / 11 / 23 / 11 /
 // 0.3 % -- two trials per pass settle 65 % of the steps in one pass and 99.7 % in two (tuned by sweep).
+// The kernel is bound by the re-reads of the 120-byte match records, so a candidate whose previous step
+// needed trial >= 2 opens with four trials in its first pass (how the trials are batched does not
+// change which one is accepted).
 #ifndef PX_HALVE_NT
 #define PX_HALVE_NT 2
 #endif
+#define PX_HALVE_NTMAX 4
 __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineArgs a, int it) {
-  constexpr int NT = PX_HALVE_NT;
-  __shared__ __align__(16) double sm_pose[4][NT][12];
-  __shared__ __align__(16) double sm_term[4][NT][32];
+  constexpr int NTMAX = PX_HALVE_NTMAX;
+  __shared__ __align__(16) double sm_pose[4][NTMAX][12];
+  __shared__ __align__(16) double sm_term[4][NTMAX][32];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + wid;
   if (c >= a.src.n) return;
@@ -923,10 +927,11 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
 #pragma unroll
   for (int q = 0; q < 6; ++q) xi[q] = pose[12 + q];
   const double f0 = pose[18];
-  const int my = lane % NT;  // the trial of the pass whose pose this lane builds and whose sum it carries
   int acc_s = -1, acc_tr = 0;
   double f_acc = 0.0;
-  for (int tr0 = 0; tr0 < 9 && acc_s < 0; tr0 += NT) {
+  int NT = st[ST_LASTTR] >= PX_HALVE_NT ? NTMAX : PX_HALVE_NT;  // trials in the first pass (a power of two)
+  for (int tr0 = 0; tr0 < 9 && acc_s < 0; tr0 += NT, NT = PX_HALVE_NT) {
+    const int my = lane & (NT - 1);  // the trial of the pass whose pose this lane builds and whose sum it carries
     {
       double r[9], t[3], rs[9];
 #pragma unroll
@@ -959,7 +964,8 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
       const int k = base + lane;
       const bool have = k < nc;
 #pragma unroll
-      for (int s_ = 0; s_ < NT; ++s_) {
+      for (int s_ = 0; s_ < NTMAX; ++s_) {
+        if (s_ >= NT) break;
         double term = 0.0;
         if (have) {
           const double* P = sm_pose[wid][s_];
@@ -989,9 +995,9 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
       __syncwarp();
     }
 #pragma unroll
-    for (int s_ = NT - 1; s_ >= 0; --s_) {  // first acceptable trial in trial order
+    for (int s_ = NTMAX - 1; s_ >= 0; --s_) {  // first acceptable trial in trial order
       const double fs = shfl_d(f, s_);
-      if (tr0 + s_ < 9 && isfinite(fs) && fs <= f0) acc_s = s_, acc_tr = tr0 + s_, f_acc = fs;
+      if (s_ < NT && tr0 + s_ < 9 && isfinite(fs) && fs <= f0) acc_s = s_, acc_tr = tr0 + s_, f_acc = fs;
     }
   }
   int failure = F_OK, conv = 0;
@@ -1020,7 +1026,7 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
   }
   if (lane == 0) {
     if (failure != F_OK) st[ST_FAIL] = failure;
-    if (failure == F_OK) st[ST_NTRACE] = it;  // an accepted step was recorded
+    if (failure == F_OK) st[ST_NTRACE] = it, st[ST_LASTTR] = acc_tr;  // an accepted step was recorded
     if (conv) st[ST_CONV] = 1;
     if (done || it >= cfg.max_iter) st[ST_DONE] = 1;
   }
