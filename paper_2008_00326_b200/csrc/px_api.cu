@@ -291,7 +291,7 @@ int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   CU(ctx->st_i.ensure(sizeof(int32_t) * 8 * (size_t)std::max<int64_t>(n_cand, 1)));
   ctx->refine_plane = (long long)tot;
   CU(ctx->src_cov.ensure(sizeof(double) * 9 * tot));
-  CU(ctx->w_buf.ensure(sizeof(double) * 15 * tot));
+  CU(ctx->w_buf.ensure(sizeof(double) * 10 * tot));
   CU(ctx->corr.ensure(sizeof(int32_t) * tot));
   return 0;
 }
@@ -1201,7 +1201,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   long long total = 0;
   if (timed) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (int r = size_clouds(ctx, ctx->clouds, slot, pose_in, n, &total)) return r;
-  const long long per_slot = 60 + (cfg->refine ? 200 : 0);
+  const long long per_slot = 60 + (cfg->refine ? 160 : 0);
   if (total * per_slot > ctx->scratch_budget && n > 1024) {
     const int64_t mid = lo + n / 2;
     if (int r = search_range(ctx, cfg, lo, mid)) return r;

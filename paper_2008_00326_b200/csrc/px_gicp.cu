@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   const int n = v.n;
   const double* soa = a.src_soa + v.off;  // planes x, y, z, v0x, v0y, v0z
   const long long plane = a.plane;
-  double* wb = a.w_buf + v.off;           // 15 compact planes
+  double* wb = a.w_buf + v.off;           // 10 compact planes
   int32_t* corr = a.corr + v.off;
   const int32_t* nn = a.nn + v.off;
   const double* tsoa = a.tgt.soa + v.toff;  // same six planes of the target
@@ -845,8 +845,8 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
       double* o = wb + *n_corr_sm + __popc(onm & ((1u << lane) - 1u));
 #pragma unroll
       for (int q = 0; q < 9; ++q) __stcs(o + q * plane, w[q]);  // streamed: read once, by the halving kernel
-      __stcs(o + 9 * plane, ax), __stcs(o + 10 * plane, ay), __stcs(o + 11 * plane, az);
-      __stcs(o + 12 * plane, tx), __stcs(o + 13 * plane, ty), __stcs(o + 14 * plane, tz);
+      // tenth plane: (source index, target index) -- the halving kernel fetches the two points itself
+      __stcs(reinterpret_cast<long long*>(o + 9 * plane), (long long)(unsigned)i | ((long long)bj << 32));
     }
     __syncwarp();
     if (lane == 0) *n_corr_sm += __popc(onm);
@@ -920,7 +920,10 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
   if (st[ST_DONE]) return;
   const GicpCfgDev cfg = a.cfg;
   const long long plane = a.plane;
-  const double* wb = a.w_buf + a.src.offset[c];
+  const double* wb = a.w_buf + a.src.offset[c];  // 10 compact planes: W (9), (source index, target index)
+  const double* soa = a.src_soa + a.src.offset[c];
+  const double* tsoa = a.tgt.soa + a.tgt.offset[a.target_idx[c]];
+  const long long tplane = a.tgt.plane;
   const int nc = st[ST_NCOMPACT];
   double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
   double xi[6];
@@ -955,10 +958,16 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
     }
     // ---- fixed-association objective (registration.py:387-407) of the NT trial poses ----
     double f = 0.0;
-    double cur[15];
+    double cur[15];  // W (9) | source point (3) | target point (3)
+    // software pipeline: the (source, target) index pair of a chunk is fetched one chunk ahead of its operands
+    long long ij_cur = lane < nc ? __ldcs(reinterpret_cast<const long long*>(wb + 9 * plane) + lane) : 0;
+    long long ij_next = lane + 32 < nc ? __ldcs(reinterpret_cast<const long long*>(wb + 9 * plane) + lane + 32) : 0;
     if (lane < nc) {
+      const int si = (int)(unsigned)ij_cur, tj = (int)(ij_cur >> 32);
 #pragma unroll
-      for (int q = 0; q < 15; ++q) cur[q] = __ldcs(wb + q * plane + lane);
+      for (int q = 0; q < 9; ++q) cur[q] = __ldcs(wb + q * plane + lane);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
     }
     for (int base = 0; base < nc; base += 32) {
       const int k = base + lane;
@@ -981,9 +990,14 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
         sm_term[wid][s_][lane] = term;
       }
       __syncwarp();
+      ij_cur = ij_next;
+      ij_next = k + 64 < nc ? __ldcs(reinterpret_cast<const long long*>(wb + 9 * plane) + k + 64) : 0;
       if (k + 32 < nc) {  // next chunk's operands are in flight during the ordered sums
+        const int si = (int)(unsigned)ij_cur, tj = (int)(ij_cur >> 32);
 #pragma unroll
-        for (int q = 0; q < 15; ++q) cur[q] = __ldcs(wb + q * plane + k + 32);
+        for (int q = 0; q < 9; ++q) cur[q] = __ldcs(wb + q * plane + k + 32);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
       }
       const double2* s2 = reinterpret_cast<const double2*>(sm_term[wid][my]);
 #pragma unroll

@@ -177,7 +177,7 @@ struct RefineArgs {
   // scratch, indexed by the source slot offsets; structure-of-arrays with plane stride `plane`
   long long plane;            // >= sum cap
   double* src_soa;            // 6 planes: x, y, z and the covariance normal v0 of every source point
-  double* w_buf;              // 15 planes, matched points compacted in index order: W = (Cb + R Ca R^T)^-1 (9), source point (3), target point (3)
+  double* w_buf;              // 10 planes, matched points compacted in index order: W = (Cb + R Ca R^T)^-1 (9), packed (source index | target index << 32)
   int32_t* corr;              // (sum cap) correspondences of the last linearisation
   int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration
   double* st_pose;            // (n,20) current iterate [R (9) | t (3)], step xi (6), f0, pad
