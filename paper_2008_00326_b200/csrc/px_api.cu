@@ -290,9 +290,8 @@ int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   CU(ctx->st_pose.ensure(sizeof(double) * 20 * (size_t)std::max<int64_t>(n_cand, 1)));
   CU(ctx->st_i.ensure(sizeof(int32_t) * 8 * (size_t)std::max<int64_t>(n_cand, 1)));
   ctx->refine_plane = (long long)tot;
-  CU(ctx->src_cov.ensure(sizeof(double) * 9 * tot));
+  CU(ctx->src_cov.ensure(sizeof(double) * 6 * tot));  // x y z + covariance normal
   CU(ctx->w_buf.ensure(sizeof(double) * 10 * tot));
-  CU(ctx->corr.ensure(sizeof(int32_t) * tot));
   return 0;
 }
 
@@ -1041,7 +1040,7 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
     a.init_T = init_T ? dinit.as<double>() : nullptr;
     a.cfg = gicp_dev(*cfg);
     a.cam = ctx->cam;
-    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>();
     a.plane = ctx->refine_plane;
     a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
     a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
@@ -1201,7 +1200,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   long long total = 0;
   if (timed) CU(cudaEventRecord(ctx->ev[0], ctx->stream));
   if (int r = size_clouds(ctx, ctx->clouds, slot, pose_in, n, &total)) return r;
-  const long long per_slot = 60 + (cfg->refine ? 160 : 0);
+  const long long per_slot = 60 + (cfg->refine ? 132 : 0);  // src planes 48, W + index planes 80, nn 4
   if (total * per_slot > ctx->scratch_budget && n > 1024) {
     const int64_t mid = lo + n / 2;
     if (int r = search_range(ctx, cfg, lo, mid)) return r;
@@ -1222,7 +1221,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     a.target_idx = ctx->c_tidx.as<int32_t>() + lo;
     a.cfg = gicp_dev(cfg->gicp);
     a.cam = ctx->cam;
-    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.corr = ctx->corr.as<int32_t>();
+    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>();
     a.plane = ctx->refine_plane;
     a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
     a.out_T = ctx->r_T.as<double>() + 12 * lo;

@@ -667,7 +667,6 @@ __global__ void __launch_bounds__(128, 8) gicp_nn_kernel(RefineArgs a, int it) {
   const CandView v = cand_view(a, c);
   const double* soa = a.src_soa + v.off;
   const long long plane = a.plane;
-  const int32_t* corr = a.corr + v.off;
   int32_t* nn = a.nn + v.off;
   double r[9], t[3];
 #pragma unroll
@@ -682,7 +681,8 @@ __global__ void __launch_bounds__(128, 8) gicp_nn_kernel(RefineArgs a, int it) {
     const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
     double best;
     int bj;
-    nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, it == 1 ? -1 : corr[i], gate2, best, bj);
+    // seed: this point's gated neighbour of the previous iteration (read before it is overwritten)
+    nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, it == 1 ? -1 : nn[i], gate2, best, bj);
     nn[i] = (bj >= 0 && !(best > gate2)) ? bj : -1;  // registration.py:261
 #ifdef PX_NN_STATS
     {
@@ -718,7 +718,6 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   const double* soa = a.src_soa + v.off;  // planes x, y, z, v0x, v0y, v0z
   const long long plane = a.plane;
   double* wb = a.w_buf + v.off;           // 10 compact planes
-  int32_t* corr = a.corr + v.off;
   const int32_t* nn = a.nn + v.off;
   const double* tsoa = a.tgt.soa + v.toff;  // same six planes of the target
   const double f_src = 1.0 - a.cfg.eps, f_tgt = a.tgt.f;
@@ -839,7 +838,6 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
         stage[(30 + u) * STAGE_LD + lane] = -wj[2][u];
       }
     }
-    if (i < n) corr[i] = on ? bj : -1;
     const unsigned onm = __ballot_sync(0xffffffffu, on);
     if (on) {  // ordered compaction for the halving kernel
       double* o = wb + *n_corr_sm + __popc(onm & ((1u << lane) - 1u));

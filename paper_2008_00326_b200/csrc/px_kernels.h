@@ -178,8 +178,7 @@ struct RefineArgs {
   long long plane;            // >= sum cap
   double* src_soa;            // 6 planes: x, y, z and the covariance normal v0 of every source point
   double* w_buf;              // 10 planes, matched points compacted in index order: W = (Cb + R Ca R^T)^-1 (9), packed (source index | target index << 32)
-  int32_t* corr;              // (sum cap) correspondences of the last linearisation
-  int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration
+  int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration (next iteration's search seeds)
   double* st_pose;            // (n,20) current iterate [R (9) | t (3)], step xi (6), f0, pad
   int32_t* st_i;              // (n,8) per-candidate integer state (px_gicp.cu: ST_*)
   // outputs
