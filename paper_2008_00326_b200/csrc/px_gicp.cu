@@ -713,7 +713,10 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(128, 8) gicp_nn_kernel(RefineArgs a, int it) {
+#ifndef PX_NN_MINB
+#define PX_NN_MINB 8
+#endif
+__global__ void __launch_bounds__(128, PX_NN_MINB) gicp_nn_kernel(RefineArgs a, int it) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + wid;
   if (c >= a.src.n) return;
