@@ -716,9 +716,12 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
 #ifndef PX_NN_MINB
 #define PX_NN_MINB 8
 #endif
-__global__ void __launch_bounds__(128, PX_NN_MINB) gicp_nn_kernel(RefineArgs a, int it) {
+// `split` warps share a candidate (its queries dealt round-robin in chunks of 32): small batches do not fill
+// the GPU with one warp per candidate, and the queries are independent.
+__global__ void __launch_bounds__(128, PX_NN_MINB) gicp_nn_kernel(RefineArgs a, int it, int split) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 4 + wid;
+  const int gw = blockIdx.x * 4 + wid;
+  const int c = gw / split, slice = gw - c * split;
   if (c >= a.src.n) return;
   if (a.st_i[8 * (size_t)c + ST_DONE]) return;
   const CandView v = cand_view(a, c);
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(128, PX_NN_MINB) gicp_nn_kernel(RefineArgs a, 
 #pragma unroll
   for (int q = 0; q < 3; ++q) t[q] = a.st_pose[ST_POSE_LD * (size_t)c + 9 + q];
   const double gate2 = a.cfg.gate2;
-  for (int i = lane; i < v.n; i += 32) {
+  for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
     const double ax = soa[i], ay = soa[plane + i], az = soa[2 * plane + i];
     const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
     const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
@@ -1225,9 +1228,14 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   cudaFuncSetAttribute(gicp_nn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all of it as L1
   const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
+  // enough NN warps for ~one full wave (148 SMs x 32 warps) when the batch is small
+#ifndef PX_NN_FILL
+#define PX_NN_FILL 4
+#endif
+  const int nn_split = (int)std::min<long long>(8, std::max<long long>(1, (148LL * 32 * PX_NN_FILL + a.src.n - 1) / a.src.n));
   for (int it = 1; it <= a.cfg.max_iter; ++it) {
     PX_MARK();
-    gicp_nn_kernel<<<b4, 128, 0, st>>>(a, it);
+    gicp_nn_kernel<<<(unsigned)(((long long)a.src.n * nn_split + 3) / 4), 128, 0, st>>>(a, it, nn_split);
     PX_MARK();
     gicp_lin_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
     PX_MARK();
