@@ -659,53 +659,65 @@ __device__ __forceinline__ void store_src_soa(double* soa, long long plane, int 
   soa[3 * plane + i] = cv[9], soa[4 * plane + i] = cv[10], soa[5 * plane + i] = cv[11];
 }
 
-__global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a) {
+// `split` (1, 2 or 4) warps of a CTA share a candidate: small batches do not fill the GPU with one warp each.
+__global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a, int split) {
   extern __shared__ __align__(16) double sm[];  // per warp: [k][32] doubles + [k][32] ints of neighbour lists
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * 4 + wid;
-  if (c >= a.src.n) return;
-  const CandView v = cand_view(a, c);
+  const int c = (blockIdx.x * 4 + wid) / split, slice = wid % split;
+  const bool live = c < a.src.n;
   const GicpCfgDev cfg = a.cfg;
+  CandView v{};
+  bool too_few = true;
+  if (live) {
+    v = cand_view(a, c);
+    too_few = v.n <= cfg.k_cov || v.nt <= cfg.k_cov;  // registration.py:504-510
+    if (slice == 0) {
+      int* st = a.st_i + 8 * (size_t)c;
+      double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
+      if (lane < 12) {
+        double val = (lane == 0 || lane == 4 || lane == 8) ? 1.0 : 0.0;  // [R | t] as 9 + 3
+        if (a.init_T) {
+          const double* T0 = a.init_T + 12 * (size_t)c;
+          val = lane < 9 ? T0[4 * (lane / 3) + lane % 3] : T0[4 * (lane - 9) + 3];
+        }
+        pose[lane] = val;
+      }
+      if (lane < 8) st[lane] = lane == ST_FAIL ? (too_few ? F_TOO_FEW : F_OK) : (lane == ST_DONE ? (too_few || cfg.max_iter < 1) : 0);
+    }
+  }
+  const bool work = live && !too_few;
   const double* src = a.src.points + 3 * v.off;
   double* soa = a.src_soa + v.off;  // planes x, y, z, v0x, v0y, v0z
   const long long plane = a.plane;
-  int* st = a.st_i + 8 * (size_t)c;
-  double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
-  if (lane < 12) {
-    double val = (lane == 0 || lane == 4 || lane == 8) ? 1.0 : 0.0;  // [R | t] as 9 + 3
-    if (a.init_T) {
-      const double* T0 = a.init_T + 12 * (size_t)c;
-      val = lane < 9 ? T0[4 * (lane / 3) + lane % 3] : T0[4 * (lane - 9) + 3];
-    }
-    pose[lane] = val;
-  }
-  const bool too_few = v.n <= cfg.k_cov || v.nt <= cfg.k_cov;  // registration.py:504-510
-  if (lane < 8) st[lane] = lane == ST_FAIL ? (too_few ? F_TOO_FEW : F_OK) : (lane == ST_DONE ? (too_few || cfg.max_iter < 1) : 0);
-  if (too_few) return;
   if (a.src.slot_map) {
-    const int4 bb = a.src.bbox[c];
-    OrgView V{src, a.src.slot_map + v.off, bb.z, bb.w};
+    int4 bb = make_int4(0, 0, 0, 0);
+    double* G = a.w_buf + v.off;  // dense copy of the cloud over its screen box, in the (still unused) match scratch
+    if (work) {
+      bb = a.src.bbox[c];
+      const int32_t* map = a.src.slot_map + v.off;
+      for (int cell = slice * 32 + lane; cell < bb.z * bb.w; cell += 32 * split) {
+        const int j = map[cell];
+        G[cell] = j >= 0 ? src[3 * j] : CUDART_NAN, G[plane + cell] = j >= 0 ? src[3 * j + 1] : CUDART_NAN;
+        G[2 * plane + cell] = j >= 0 ? src[3 * j + 2] : CUDART_NAN;
+      }
+    }
+    __syncthreads();  // the warps of a candidate read each other's part of the grid (uniform: no early exits above)
+    if (!work) return;
+    const int32_t* map = a.src.slot_map + v.off;
     const int32_t* spx = a.src.src_px + 2 * v.off;
     const int stp = a.cam.stride;
     double* nd = sm + (size_t)wid * (cfg.k_cov * 48) + lane;
     int* ni = reinterpret_cast<int*>(sm + (size_t)wid * (cfg.k_cov * 48) + cfg.k_cov * 32) + lane;
-    // dense copy of the cloud over its screen box, in the match scratch (unused until the first linearisation)
-    double* G = a.w_buf + v.off;
-    for (int cell = lane; cell < bb.z * bb.w; cell += 32) {
-      const int j = V.map[cell];
-      G[cell] = j >= 0 ? src[3 * j] : CUDART_NAN, G[plane + cell] = j >= 0 ? src[3 * j + 1] : CUDART_NAN;
-      G[2 * plane + cell] = j >= 0 ? src[3 * j + 2] : CUDART_NAN;
-    }
-    __syncwarp();
-    for (int i = lane; i < v.n; i += 32) {
+    for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
       double cv[12];
-      knn_ring_dense<32>(G, plane, V.map, bb.z, bb.w, src[3 * i], src[3 * i + 1], src[3 * i + 2], spx[2 * i] / stp - bb.x,
+      knn_ring_dense<32>(G, plane, map, bb.z, bb.w, src[3 * i], src[3 * i + 1], src[3 * i + 2], spx[2 * i] / stp - bb.x,
                          spx[2 * i + 1] / stp - bb.y, cfg.k_cov, a.cam.ray_k, nd, ni);
       cov_from_neighbours<32>(src, ni, cfg.k_cov, cfg.eps, cv);
       store_src_soa(soa, plane, i, src, cv);
     }
   } else {
-    for (int i = lane; i < v.n; i += 32) {
+    if (!work) return;
+    for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
       double cv[12];
       cov_point(src, v.n, i, cfg.k_cov, cfg.eps, cv);
       store_src_soa(soa, plane, i, src, cv);
@@ -1223,7 +1235,9 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
   PX_MARK();
-  gicp_init_kernel<<<b4, 128, smem_init, st>>>(a);
+  // 1, 2 or 4 warps per candidate: about two waves of 148 SMs x 24 warps when the batch is small
+  const int init_split = a.src.n >= 3552 ? 1 : (a.src.n >= 1776 ? 2 : 4);
+  gicp_init_kernel<<<(unsigned)(((long long)a.src.n * init_split + 3) / 4), 128, smem_init, st>>>(a, init_split);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   cudaFuncSetAttribute(gicp_nn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all of it as L1
