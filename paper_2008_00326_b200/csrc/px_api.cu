@@ -156,10 +156,14 @@ int sync_models(px_ctx* ctx) {
 
 int slots_from_ids(px_ctx* ctx, const int32_t* ids, int64_t n, std::vector<int32_t>& out) {
   out.resize((size_t)n);
+  int32_t last_id = 0, last_slot = -1;  // candidates come in runs of one object
   for (int64_t i = 0; i < n; ++i) {
-    auto it = ctx->slot_of.find(ids[i]);
-    if (it == ctx->slot_of.end()) return fail(ctx, PX_E_ARG, "no model registered for id " + std::to_string(ids[i]));
-    out[(size_t)i] = it->second;
+    if (last_slot < 0 || ids[i] != last_id) {
+      auto it = ctx->slot_of.find(ids[i]);
+      if (it == ctx->slot_of.end()) return fail(ctx, PX_E_ARG, "no model registered for id " + std::to_string(ids[i]));
+      last_id = ids[i], last_slot = it->second;
+    }
+    out[(size_t)i] = last_slot;
   }
   return 0;
 }

@@ -218,10 +218,14 @@ class SearchPlan:
     def rank_in_object(self) -> np.ndarray:
         """Position of each candidate among its object's candidates: the index
         `select_best` ranks by (search.py:178-183, 346-360)."""
+        cached = getattr(self, "_rank_cache", None)
+        if cached is not None and cached.shape[0] == self.n:
+            return cached
         rank = np.empty(self.n, dtype=np.int32)
         for oid in self.active:
             sel = np.nonzero(self.flat_oid == oid)[0]
             rank[sel] = np.arange(sel.size, dtype=np.int32)
+        self._rank_cache = rank
         return rank
 
 

@@ -7,7 +7,7 @@ import bench
 import numpy as np
 from paper_2008_00326_b200.engine import Engine
 wl = sys.argv[1] if len(sys.argv) > 1 else "c3"
-frame, models, cfg, plan = bench.build_workload(wl, 1, 1)
+frame, models, cfg, plan = bench.build_workload(wl, 1, 1, materialise_targets=False)
 eng = Engine(0)
 idx = np.arange(plan.n)
 sc = eng.search_cfg(plan)
@@ -16,7 +16,7 @@ for rep in range(3):
     eng._scene_key = None; eng._model_keys.clear()
     eng.upload_scene(frame, plan.cfg.stride, plan.observed, plan.obs_labels); eng.sync(); t.append(time.perf_counter())
     eng.upload_models({oid: models[oid] for oid in plan.active}); eng.sync(); t.append(time.perf_counter())
-    eng.upload_targets(plan.target_offsets, plan.target_points, plan.cfg.gicp, plan.target_obs_index); eng.sync(); t.append(time.perf_counter())
+    eng.build_targets(plan); eng.sync(); t.append(time.perf_counter())
     n = eng.search_upload(plan, idx); eng.sync(); t.append(time.perf_counter())
     eng.search_run(sc); eng.sync(); t.append(time.perf_counter())
     out = eng.search_download(n); t.append(time.perf_counter())
