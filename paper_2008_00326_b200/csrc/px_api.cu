@@ -903,7 +903,7 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   CU(ctx->tgt_org.ensure(n1 * sizeof(TgtOrg)));
   CU(ctx->tgt_world.ensure((size_t)std::max<int64_t>(ctx->n_obs, 1) * 24));
   a.obs_pts = ctx->obs_pts.as<double>(), a.obs_labels = ctx->obs_labels.as<int32_t>();
-  a.obs_cell = ctx->obs_cell.as<int32_t>(), a.n_obs = ctx->n_obs, a.GW = ctx->cam.GW;
+  a.obs_cell = ctx->obs_cell.as<int32_t>(), a.gidx = ctx->gidx.as<int32_t>(), a.n_obs = ctx->n_obs, a.GW = ctx->cam.GW;
   a.world = ctx->tgt_world.as<double>();
   a.cnt = ctx->tgt_sizes.as<long long>(), a.cells = a.cnt + n1, a.nodes = a.cells + n1;
   long long* off = ctx->tgt_off.as<long long>();

@@ -124,6 +124,7 @@ struct TgtBuildArgs {
   const double* obs_pts;      // (n_obs,3) camera frame
   const int32_t* obs_labels;  // (n_obs)
   const int32_t* obs_cell;    // (n_obs) stride-grid cell gy*GW+gx of every observed point
+  const int32_t* gidx;        // (GH*GW) observed index of every stride-grid cell or -1
   long long n_obs;
   int GW;
   double* world;              // scratch: 3 planes of n_obs (mode 0)

@@ -93,9 +93,14 @@ __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int run = 0;
   double m = 0.0;
-  for (long long base = 0; base < a.n_obs; base += blockDim.x) {
-    const long long i = base + threadIdx.x;
-    const bool in = i < a.n_obs && tgt_member(a, t, i, prm);
+  // only the cells of the target's grid bounding box (pass 1) can hold members; row-major cell order is
+  // ascending observed index, the order np.nonzero returns
+  const int ncell = a.cnt[t] > 0 ? o.w * o.h : 0;
+  for (int base = 0; base < ncell; base += blockDim.x) {
+    const int lc = base + (int)threadIdx.x;
+    long long i = -1;
+    if (lc < ncell) i = a.gidx[(lc / o.w + o.gy0) * a.GW + lc % o.w + o.gx0];
+    const bool in = i >= 0 && tgt_member(a, t, i, prm);
     const unsigned bal = __ballot_sync(0xffffffffu, in);
     if (lane == 0) wcnt[w] = __popc(bal);
     __syncthreads();
@@ -109,8 +114,6 @@ __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
       const double x = a.obs_pts[3 * i], y = a.obs_pts[3 * i + 1], z = a.obs_pts[3 * i + 2];
       a.tgt_obs[off + pos] = (int32_t)i;
       a.tgt_pts[3 * (off + pos)] = x, a.tgt_pts[3 * (off + pos) + 1] = y, a.tgt_pts[3 * (off + pos) + 2] = z;
-      const int cell = a.obs_cell[i];
-      const int lc = (cell / a.GW - o.gy0) * o.w + (cell % a.GW - o.gx0);
       a.tpix[off + pos] = lc;
       a.tmap[o.map_off + lc] = pos;
       m = fmax(m, fmax(fabs(x), fmax(fabs(y), fabs(z))));
