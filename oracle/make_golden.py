@@ -220,6 +220,20 @@ def scene_c3():
     return disk_roundtrip(sg.generate_scene(spec, models)), models
 
 
+def scene_c3_noisy():
+    """C3's scene with the sensor noise model of SURVEY.md 8(d): depth sigma 2 mm, 2 % dropout, colour
+    jitter 0.02 (scenegen.apply_noise, default_rng(seed)) -- holes in the organised clouds, jittered colours."""
+    k = sg.make_camera(640, 480)
+    dims = [(0.046, 0.036, 0.09), (0.06, 0.04, 0.12), (0.05, 0.05, 0.07), (0.08, 0.03, 0.10), (0.04, 0.03, 0.15)]
+    cols = [((0.75, 0.65, 0.1), (0.2, 0.2, 0.55)), ((0.8, 0.1, 0.1), (0.9, 0.8, 0.7)), ((0.1, 0.6, 0.2), (0.1, 0.2, 0.1)),
+            ((0.1, 0.3, 0.8), (0.8, 0.8, 0.2)), ((0.6, 0.2, 0.7), (0.2, 0.7, 0.7))]
+    models = {i + 1: sg.build_model(i + 1, sg.PrimitiveSpec("box", dims[i], ((0.0, 0.5, cols[i][0]), (0.5, 1.0, cols[i][1]))))
+              for i in range(5)}
+    spec = sg.random_scene_spec(models, seed=11, placement_extent=(0.2, 0.2), intrinsics=k)
+    frame = sg.apply_noise(sg.generate_scene(spec, models), sg.NoiseModel(0.002, 0.02, 0.02), seed=7)
+    return disk_roundtrip(frame), models
+
+
 def scene_c4():
     k = sg.make_camera(640, 480)
     models = sg.mixed_object_suite()
@@ -344,7 +358,7 @@ def tiny_dataset():
 
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
-    which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c4", "tiny"}
+    which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c3n", "c4", "tiny"}
     if "tiny" in which:
         tiny_dataset()
     if "units" in which:
@@ -364,6 +378,11 @@ def main():
         search_fixture("c3_clutter_3dof", frame, models,
                        rs.SearchConfig(mode="3dof", workspace=(-0.32, 0.32, -0.32, 0.32), dt=0.02,
                                        max_proposals=1500, workers=WORKERS), keep_every=211)
+    if "c3n" in which:
+        frame, models = scene_c3_noisy()
+        search_fixture("c3n_clutter_noisy", frame, models,
+                       rs.SearchConfig(mode="3dof", workspace=(-0.32, 0.32, -0.32, 0.32), dt=0.02,
+                                       max_proposals=700, workers=WORKERS), keep_every=233)
     if "c4" in which:
         frame, models = scene_c4()
         search_fixture("c4_mixed_6dof", frame, models,

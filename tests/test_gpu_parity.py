@@ -127,7 +127,7 @@ def test_m2m_gicp_failure_slots(engine):
     assert out[2].failure == "degenerate_correspondences" and out[2].iterations == 1
 
 
-SEARCH = ["c1_box_3dof", "c2_twocyl_color1", "c2_twocyl_color0", "c3_clutter_3dof", "c4_mixed_6dof"]
+SEARCH = ["c1_box_3dof", "c2_twocyl_color1", "c2_twocyl_color0", "c3_clutter_3dof", "c3n_clutter_noisy", "c4_mixed_6dof"]
 
 
 @pytest.mark.parametrize("name", SEARCH)

@@ -121,7 +121,7 @@ def test_gicp_align_matches_reference(t):
 
 # ---- whole-path fixtures ---------------------------------------------------------------
 
-SEARCH = ["c1_box_3dof", "c2_twocyl_color1", "c2_twocyl_color0", "c3_clutter_3dof", "c4_mixed_6dof"]
+SEARCH = ["c1_box_3dof", "c2_twocyl_color1", "c2_twocyl_color0", "c3_clutter_3dof", "c3n_clutter_noisy", "c4_mixed_6dof"]
 
 
 @pytest.mark.parametrize("name", SEARCH)
