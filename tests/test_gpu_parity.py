@@ -467,3 +467,48 @@ def test_full_size_determinism_chunking_and_sharding(engine):
     for slot, oid in enumerate(plan.active):
         e = res.estimate_for(oid)
         assert (int(merged[slot]) >> 32, int(merged[slot]) & 0xffffffff) == (e.cost.total, e.proposal_index)
+
+
+def _adds(mesh_pts, pose_a, pose_b):
+    """ADD-S: mean distance from every model point under pose_a to the closest model point under pose_b."""
+    a = mesh_pts @ pose_a.rotation.T + pose_a.translation
+    b = mesh_pts @ pose_b.rotation.T + pose_b.translation
+    d = ((a[:, None, :] - b[None, :, :]) ** 2).sum(-1)
+    return float(np.sqrt(d.min(axis=1)).mean())
+
+
+def test_reference_search_tests_through_public_api(engine):
+    """The reference's own search-level tests (pkg/tests/test_search.py:151-245) replayed on the
+    committed two-cylinder scene through estimate_poses: recovery within 1 cm with colour on,
+    refinement never worse than no refinement, small 6-DoF search with the in-plane axis collapsed
+    for symmetric models, failures reported per object, uniform subsampling by max_proposals, and
+    timing kept out of the result JSON."""
+    from paper_2008_00326_b200 import SearchConfig, estimate_poses, timings_to_json
+    d, frame, models, cfg, plan = G.scene("c2_twocyl_color1")
+    gt = {s.object_id: s.pose for s in frame.ground_truth}
+    ws = (-0.32, 0.32, -0.32, 0.32)
+    # :151-161 colour on separates the same-shape objects
+    res = estimate_poses(frame, models, SearchConfig(mode="3dof", workspace=ws, dt=0.1))
+    for e in res.estimates:
+        assert not e.failed and _adds(models[e.object_id].mesh.vertices, gt[e.object_id], e.pose) < 0.01
+    # :183-192 refinement never increases the winning cost
+    off = estimate_poses(frame, models, SearchConfig(mode="3dof", workspace=ws, dt=0.1, refine=False))
+    for on_e, off_e in zip(res.estimates, off.estimates):
+        assert on_e.cost.total <= off_e.cost.total
+    # :195-209 6-DoF, yaw-symmetric models collapse n_inplane
+    r1 = estimate_poses(frame, models, SearchConfig(mode="6dof", viewpoints=16, n_inplane=1))
+    r16 = estimate_poses(frame, models, SearchConfig(mode="6dof", viewpoints=16, n_inplane=16))
+    assert r16.proposals_evaluated == r1.proposals_evaluated
+    for e in r1.estimates:
+        assert not e.failed and _adds(models[e.object_id].mesh.vertices, gt[e.object_id], e.pose) < 0.02
+    # :212-220 failures are per object
+    one = estimate_poses(frame, {1: models[1]}, SearchConfig(mode="3dof", workspace=ws, dt=0.1))
+    by_id = {e.object_id: e for e in one.estimates}
+    assert by_id[2].failed and by_id[2].failure == "unknown_object" and not by_id[1].failed
+    # :223-233 timing stays out of the result JSON
+    assert "millis" not in result_to_json(res)
+    t = json.loads(timings_to_json(res))
+    assert t["total_millis"] > 0 and set(t["stage_millis"]) == {"render", "refine", "rerender", "cost"}
+    # :236-242 uniform subsample
+    sub = estimate_poses(frame, models, SearchConfig(mode="3dof", workspace=ws, dt=0.05, max_proposals=20))
+    assert sub.proposals_evaluated == 20
