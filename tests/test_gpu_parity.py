@@ -512,3 +512,47 @@ def test_reference_search_tests_through_public_api(engine):
     # :236-242 uniform subsample
     sub = estimate_poses(frame, models, SearchConfig(mode="3dof", workspace=ws, dt=0.05, max_proposals=20))
     assert sub.proposals_evaluated == 20
+
+
+def test_randomised_units_against_oracle(engine):
+    """Seeded random sweeps, device vs the pinned oracle, everything bit-exact: kNN (random and
+    integer-lattice clouds with many exact ties, k up to 8), rendered cost (colour on/off, clouds
+    from 1 to 200 points), covariances (flat, noisy and duplicate-heavy clouds) and single-view
+    z-buffers of random meshes -- the randomised halves of the reference's unit tests
+    (tests/test_neighbors.py:54-84, test_cost.py:102-125, test_registration.py:59-78,
+    test_raster.py:68-80)."""
+    rng = np.random.default_rng(20260117)
+    for trial in range(40):
+        nq, nt, k = int(rng.integers(1, 70)), int(rng.integers(1, 90)), int(rng.integers(1, 9))
+        if trial % 2:
+            q, t = rng.integers(-3, 4, (nq, 3)).astype(float), rng.integers(-3, 4, (nt, 3)).astype(float)
+        else:
+            q, t = rng.normal(size=(nq, 3)), rng.normal(size=(nt, 3))
+        gi, gd = engine.knn(q, t, k)
+        oi, od = O.knn(q, t, k)
+        assert np.array_equal(gi, oi) and np.array_equal(gd, od), trial
+    for trial in range(40):
+        nr, no = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+        rp, op = rng.normal(scale=0.03, size=(nr, 3)), rng.normal(scale=0.03, size=(no, 3))
+        rl, ol = rng.uniform(0, 100, (nr, 3)) * [1, 0.6, 0.6], rng.uniform(0, 100, (no, 3)) * [1, 0.6, 0.6]
+        delta, tau, uc = float(rng.uniform(0.005, 0.03)), float(rng.uniform(5, 40)), bool(trial % 2)
+        z2 = lambda n: np.zeros((n, 2), dtype=np.int32)
+        jr, ex = cost.rendered_cost(LabeledCloud(rp, rl, z2(nr)), LabeledCloud(op, ol, z2(no)), CostParams(delta, tau, uc))
+        ojr, oex = O.rendered_cost(rp, rl, op, ol, delta, tau, uc)
+        assert jr == ojr and np.array_equal(ex, oex.astype(bool)), trial
+    for trial in range(12):
+        n = int(rng.integers(25, 400))
+        pts = rng.normal(size=(n, 3)) * [0.1, 0.1, 0.002 if trial % 3 == 0 else 0.05]
+        if trial % 4 == 3:
+            pts[n // 2:] = pts[: n - n // 2]  # exact duplicates: zero distances and ties
+        assert np.array_equal(engine.covariances(pts, 20, 1e-3), O.covariances(pts)), trial
+    for trial in range(6):
+        nv = int(rng.integers(4, 40))
+        v = rng.uniform(-0.06, 0.06, (nv, 3))
+        tris = rng.integers(0, nv, (int(rng.integers(1, 120)), 3)).astype(np.int32)  # may contain degenerate faces
+        mesh = TriangleMesh(v, rng.uniform(0, 1, (nv, 3)), tris)
+        pose = np.hstack([np.eye(3), [[0.0], [0.0], [0.35]]])
+        z, cb, valid, owner = engine.rasterize_mesh(mesh, RigidTransform.from_matrix3x4(pose), K64)
+        oz, oc, ov, oo = O.rasterize(O.OracleModel(1, mesh), pose, K64)
+        assert np.array_equal(valid, ov) and np.array_equal(z, oz) and np.array_equal(owner, oo), trial
+        assert np.array_equal(cb[valid], oc[ov])
