@@ -153,9 +153,17 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knobs (one-GPU boxes): PX_BENCH_DEVICE pins every rank to one device, PX_BENCH_BACKEND=gloo replaces
+    # NCCL (which refuses two ranks on one GPU) so the multi-rank code path can be exercised end to end
+    local = int(os.environ.get("PX_BENCH_DEVICE", local))
+    backend = os.environ.get("PX_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     peaks = {}
     pk = ROOT / "MEASURED_PEAKS.json"
     if pk.exists():
@@ -178,7 +186,7 @@ def run_gpu(args):
             dist.barrier()
             torch.cuda.synchronize()
 
-    keys_t = torch.zeros(max(len(plan.active), 1), dtype=torch.int64, device="cuda")
+    keys_t = torch.zeros(max(len(plan.active), 1), dtype=torch.int64, device=coll_dev)
 
     def reduce_keys(out):
         """The only collective: min over ranks of (total << 32 | rank-in-object) per object."""
@@ -217,10 +225,10 @@ def run_gpu(args):
     clocks = sampler.stop() if sampler else None
     total_ms = float(np.sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([total_ms], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-        cnt = torch.tensor([n_local], dtype=torch.int64, device="cuda")
+        cnt = torch.tensor([n_local], dtype=torch.int64, device=coll_dev)
         dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
         n_total = int(cnt.item())
     else:
@@ -253,7 +261,7 @@ def run_gpu(args):
     d2h = n_local * (96 + 96 + 4 * 6) + 8 * len(plan.active)
     e2e_t = float(np.median(e2e_ms)) * 1e-3
     if world > 1:
-        t = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_t = float(t.item())
     e2e_value = n_total / e2e_t
