@@ -577,3 +577,22 @@ def test_full_size_sample_against_oracle(engine):
           f"costs-equal={same.mean():.4f}")
     assert close.mean() >= 0.99 and (dev.iterations == cpu.iterations).mean() >= 0.99
     assert same[close].all()
+
+
+def test_full_size_6dof_sample_against_oracle(engine):
+    """BASELINE configs[3] at the size bench.py --workload c4 measures (249,738 mask-constrained 6-DoF
+    candidates): every 83rd candidate, device (label targets built on the device) vs the pinned oracle."""
+    import bench
+    frame, models, cfg, spec = bench.build_workload("c4", 1, 1, materialise_targets=False)
+    _, _, _, host = bench.build_workload("c4", 1, 1, materialise_targets=True)
+    assert spec.n == 249738
+    pick = np.arange(0, spec.n, 83)
+    dev = engine.run_plan(frame, models, spec, pick)
+    cpu = O.run_plan(frame, models, host, index=pick)
+    assert np.array_equal(dev.n_first, cpu.n_first)
+    dt, dr = G.pose_delta(dev.refined_cam, cpu.refined_cam)
+    close = (dt <= 1e-4) & (dr <= 1e-4)
+    same = (dev.j_o == cpu.j_o) & (dev.j_r == cpu.j_r)
+    print(f"full-size 6-DoF sample: n={pick.size} pose-agree={close.mean():.4f} "
+          f"iters-equal={(dev.iterations == cpu.iterations).mean():.4f} costs-equal={same.mean():.4f}")
+    assert close.mean() >= 0.99 and same[close].all()
