@@ -38,6 +38,7 @@ class Engine:
         self.device = int(device)
         self._scene_key = None
         self._model_keys = {}
+        self._model_refs = {}
         self._keep = []
 
     def close(self):
@@ -103,6 +104,7 @@ class Engine:
                                       N.ptr(tris, N.i32p), verts.shape[0], tris.shape[0], N.ptr(cyl, N.f64p))
         N.check(self.ctx, rc, "px_model_upload")
         self._model_keys[object_id] = key
+        self._model_refs[object_id] = mesh  # keeps id(mesh) from being reused while the key is cached
 
     def upload_models(self, models: dict):
         for oid, m in models.items():
