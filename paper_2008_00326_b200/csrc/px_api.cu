@@ -92,7 +92,7 @@ struct px_ctx {
   DevBuf c_slot, c_pose, c_tidx, c_rank;
   // search scratch / results
   CloudStore clouds;
-  DevBuf src_cov, w_buf, corr, nn, st_pose, st_i, total_dev;
+  DevBuf src_cov, w_buf, corr, nn, st_pose, st_i, st_hg, total_dev;
   long long refine_plane = 0;  // plane stride of the structure-of-arrays refine scratch
   DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1;
   int bitmap_slots = 0;
@@ -293,6 +293,7 @@ int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   CU(ctx->nn.ensure(sizeof(int32_t) * tot));
   CU(ctx->st_pose.ensure(sizeof(double) * 20 * (size_t)std::max<int64_t>(n_cand, 1)));
   CU(ctx->st_i.ensure(sizeof(int32_t) * 8 * (size_t)std::max<int64_t>(n_cand, 1)));
+  CU(ctx->st_hg.ensure(sizeof(double) * 44 * (size_t)std::max<int64_t>(n_cand, 1)));
   ctx->refine_plane = (long long)tot;
   CU(ctx->src_cov.ensure(sizeof(double) * 6 * tot));  // x y z + covariance normal
   CU(ctx->w_buf.ensure(sizeof(double) * 10 * tot));
@@ -342,7 +343,7 @@ void px_ctx_destroy(px_ctx* ctx) {
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
                     &ctx->obs_cell, &ctx->tgt_v0, &ctx->tgt_obs, &ctx->tgt_world, &ctx->tgt_sizes, &ctx->tgt_scans, &ctx->tgt_params,
                     &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
-                    &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->total_dev, &ctx->r_T,
+                    &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->st_hg, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
   for (DevBuf* b : bufs) b->release();
@@ -1046,7 +1047,7 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
     a.cam = ctx->cam;
     a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>();
     a.plane = ctx->refine_plane;
-    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
+    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>(), a.st_hg = ctx->st_hg.as<double>();
     a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
     a.out_resid = out_residual ? dres.as<double>() : nullptr;
     a.out_trace = out_trace ? dtr.as<double>() : nullptr;
@@ -1227,7 +1228,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
     a.cam = ctx->cam;
     a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>();
     a.plane = ctx->refine_plane;
-    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>();
+    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>(), a.st_hg = ctx->st_hg.as<double>();
     a.out_T = ctx->r_T.as<double>() + 12 * lo;
     a.out_iters = ctx->r_iters.as<int32_t>() + lo, a.out_flags = ctx->r_flags.as<int32_t>() + lo;
     a.out_ncorr_sum = ctx->r_ncorr.as<int32_t>() + lo;

@@ -943,25 +943,42 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     }
     __syncwarp();
   }
-  hg[lane] = acc0;
-  if (lane < 11) hg[32 + lane] = acc1;
-  __syncwarp();
+  // H (36), g (6), f0 go to global memory: the 6x6 solve runs in its own kernel, one THREAD per candidate
+  // (as a one-lane tail of this kernel it held the warp, its 128 registers per lane and its staging memory
+  // for ~1,000 serial instructions per candidate)
+  double* out_hg = a.st_hg + 44 * (size_t)c;
+  out_hg[lane] = acc0;
+  if (lane < 11) out_hg[32 + lane] = acc1;
   if (lane == 0) {
     const int n_corr = *n_corr_sm;
-    int failure = F_OK;
-    double xi0[6] = {0, 0, 0, 0, 0, 0};
-    if (n_corr < 6)
-      failure = F_DEGENERATE;
-    else if (solve_normal_equations(hg, hg + 36, xi0))
-      failure = F_SINGULAR;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) pose[12 + q] = xi0[q];
-    pose[18] = hg[42];
     st[ST_ITERS] = it;
     st[ST_NCORR] += n_corr;
     st[ST_NCOMPACT] = n_corr;
-    if (failure != F_OK) st[ST_FAIL] = failure, st[ST_DONE] = 1;
   }
+}
+
+// registration.py:434-437 + :479-494 for iteration `it`: degenerate / singular exits, else the step xi.
+__global__ void __launch_bounds__(128) gicp_solve_kernel(RefineArgs a) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.src.n) return;
+  int* st = a.st_i + 8 * (size_t)c;
+  if (st[ST_DONE]) return;
+  const double* hg = a.st_hg + 44 * (size_t)c;
+  double h[36], g[6], xi0[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < 36; ++q) h[q] = hg[q];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) g[q] = hg[36 + q];
+  int failure = F_OK;
+  if (st[ST_NCOMPACT] < 6)
+    failure = F_DEGENERATE;
+  else if (solve_normal_equations(h, g, xi0))
+    failure = F_SINGULAR;
+  double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) pose[12 + q] = xi0[q];
+  pose[18] = hg[42];
+  if (failure != F_OK) st[ST_FAIL] = failure, st[ST_DONE] = 1;
 }
 
 // Step halving, state update and termination tests (registration.py:443-471) for iteration `it`.
@@ -1252,6 +1269,7 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
     gicp_nn_kernel<<<(unsigned)(((long long)a.src.n * nn_split + 3) / 4), 128, 0, st>>>(a, it, nn_split);
     PX_MARK();
     gicp_lin_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
+    gicp_solve_kernel<<<(a.src.n + 127) / 128, 128, 0, st>>>(a);  // timed together with the linearisation
     PX_MARK();
     gicp_halve_kernel<<<b4, 128, 0, st>>>(a, it);
   }
@@ -1259,7 +1277,7 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   gicp_finish_kernel<<<b4, 128, 0, st>>>(a);
   PX_MARK();
 #undef PX_MARK
-  if (launches) *launches = 2 + 3 * std::max(a.cfg.max_iter, 0);
+  if (launches) *launches = 2 + 4 * std::max(a.cfg.max_iter, 0);
 #ifdef PX_NN_STATS
   cudaStreamSynchronize(st);
   dump_nn_stats();

@@ -182,6 +182,7 @@ struct RefineArgs {
   int32_t* nn;                // (sum cap) gated nearest neighbours of the current iteration (next iteration's search seeds)
   double* st_pose;            // (n,20) current iterate [R (9) | t (3)], step xi (6), f0, pad
   int32_t* st_i;              // (n,8) per-candidate integer state (px_gicp.cu: ST_*)
+  double* st_hg;              // (n,44) normal equations of the current iteration: H (36), g (6), f0, pad
   // outputs
   double* out_T;              // (n,12) [orthonormalize(R)|t]
   int32_t* out_iters;
@@ -198,7 +199,7 @@ struct RefineArgs {
   int c2w_vec_order, w2c_vec_order;
   double fixed_z;
 };
-// Launch order: init, (nn, lin, halve) x max_iter, finish.  `marks` (nullable) receives one event
+// Launch order: init, (nn, lin + solve, halve) x max_iter, finish.  `marks` (nullable) receives one event
 // before every launch and one after the last: 3 + 3 * max_iter events.
 cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, cudaEvent_t* marks = nullptr);
 
