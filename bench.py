@@ -310,7 +310,8 @@ def run_gpu(args):
         table[k] = {"launches_per_step": nl, "ms_per_step": ms, "ms_per_launch": per_launch_ms,
                     "algorithmic_bytes_per_launch": per_launch_b,
                     "achieved_gbs": per_launch_b / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0,
-                    "traffic": traffic_db.get(k, {}).get("dram_bytes_per_launch")}
+                    "traffic": traffic_db.get(k, {}).get("dram_bytes_per_launch"),
+                    "ncu": traffic_db.get(k, {}).get("ncu")}
     dom = max(table, key=lambda k: table[k]["ms_per_step"])
     dk = table[dom]
     refine_gbs = ab["refine"] / (st["refine"] * 1e-3) / 1e9 if st["refine"] > 0 else 0.0
@@ -318,6 +319,9 @@ def run_gpu(args):
                 "unit": "GB/s", "frac": dk["achieved_gbs"] / hbm_peak, "traffic": dk["traffic"],
                 "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full capture of one launch of this "
                                 "kernel on this workload (profiles/traffic.json); null when no capture matches",
+                "ncu": dk["ncu"],
+                "ncu_note": "counters of the committed ncu --set full capture of this kernel (profiles/): the true limiter "
+                            "(issue slots / lane occupancy / fp64 pipe) next to the HBM fraction asked for",
                 "algorithmic_bytes_per_launch": dk["algorithmic_bytes_per_launch"], "kernel_ms": dk["ms_per_launch"],
                 "launches_per_step": dk["launches_per_step"],
                 "timing": "CUDA events recorded on the launch stream around every launch of the GICP stage inside the timed steps",
