@@ -117,7 +117,7 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refine):
+def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refine, n_m, n_fp):
     """SURVEY.md 8(d) per-candidate algorithmic bytes, summed over the batch,
     split per kernel.  f64 = 8 B, i32 = 4 B, bool = 1 B."""
     V = np.array([models[int(o)].mesh.vertices.shape[0] for o in flat_oid], dtype=np.float64)
@@ -128,7 +128,7 @@ def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refi
     b_render1 = 96 + 48 * V + 12 * T + 13 * cap1 + 56 * n1
     b_cov = 96 * n0
     b_iter_sum = it * (104 * n0 + 344) + 96 * ncorr_sum.astype(np.float64)
-    b_cost = 56 * n1 + 48 * n1 + 25 * cap1 + 8   # n_m <= n_r, footprint ~ screen box of the final render
+    b_cost = 56 * n1 + 48 * n_m.astype(np.float64) + 25 * n_fp.astype(np.float64) + 8  # n_m, n_fp counted by cost_kernel
     d = {"render": float(b_render0.sum()), "rerender": float(b_render1.sum()) if refine else 0.0,
          "refine": float((b_cov + b_iter_sum).sum()) if refine else 0.0, "cost": float(b_cost.sum())}
     d["total"] = sum(d.values())
@@ -144,6 +144,11 @@ def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refi
         "gicp_halve_kernel": 0.0, "gicp_finish_kernel": 0.0,
     }
     return d
+
+
+def workload_string(name, cfg):
+    """Identical in both arms (the driver's same_config check compares it)."""
+    return f"{name}: {WORKLOADS[name][0]} scene, mode={cfg.mode}, refine={cfg.refine}, stride={cfg.stride}, 640x480"
 
 
 def run_gpu(args):
@@ -175,8 +180,16 @@ def run_gpu(args):
     frame, models, cfg, plan = build_workload(args.workload, world, args.scale, materialise_targets=False)
     idx = shard_index(plan, rank, world)
     eng = Engine(local)
-    stream = torch.cuda.current_stream()
+    # a non-default torch stream: its handle is non-zero, so libpx launches on exactly the stream the L2 flush and
+    # the timing events are recorded on (handle 0 would mean "the context's own stream" to px_ctx_set_stream)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
+    device_comm = world > 1 and backend == "nccl"
+    if device_comm:
+        eng.comm_init_torch()  # libpx's own NCCL communicator; the unique id travels over torch.distributed
+        if rank == 0:
+            print(f"[bench] libpx NCCL communicator up: nranks {eng.comm_world()}, NCCL {eng.nccl_version()}", file=sys.stderr)
     sc = eng.search_cfg(plan)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
@@ -188,11 +201,15 @@ def run_gpu(args):
 
     keys_t = torch.zeros(max(len(plan.active), 1), dtype=torch.int64, device=coll_dev)
 
-    def reduce_keys(out):
-        """The only collective: min over ranks of (total << 32 | rank-in-object) per object."""
-        if world > 1:
-            keys_t.copy_(torch.from_numpy(keys_from_device(plan, out.best_keys)))
+    def reduce_host(keys: dict):
+        """gloo test knob only: the min-reduction through host memory (NCCL refuses two ranks on one GPU)."""
+        if world > 1 and not device_comm:
+            keys_t.copy_(torch.from_numpy(keys_from_device(plan, keys)))
             dist.all_reduce(keys_t, op=dist.ReduceOp.MIN)
+
+    def winners_keys():
+        w = eng.search_winners()
+        return w, {o: w[o][0] for o in w}
 
     # ---- resident-input arm (`value`) ----
     eng.prepare_plan(frame, models, plan)
@@ -200,25 +217,27 @@ def run_gpu(args):
     eng.set_kernel_timing(True)  # event marks around every refine-stage launch (roofline of the dominant kernel)
     for _ in range(args.warmup):
         eng.search_run(sc)
-    out = eng.search_download(n_local)
-    reduce_keys(out)
+        eng.search_reduce()
+    reduce_host(winners_keys()[1])
     barrier()
     sampler = ClockSampler(local) if rank == 0 else None
     launches0 = eng.launch_count()
-    step_ms, stage_ms, kern_ms = [], [], []
+    step_ms, stage_ms, kern_ms, reduce_ms = [], [], [], []
     t_wall0 = time.perf_counter()
     for _ in range(args.steps):
-        flush.zero_()  # L2 flush between timed iterations (outside the event pair)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()  # L2 flush between timed iterations (outside the event pair, same stream)
+        e0, em, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        eng.search_run(sc)
+        eng.search_run(sc)      # render -> GICP -> re-render -> cost -> per-object atomicMin keys
+        em.record(stream)
+        eng.search_reduce()     # NCCL all-reduce(MIN) of the keys + winner records (device, no host sync)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
-        o = eng.search_download(n_local, full=False)
-        stage_ms.append(o.stage_millis)
+        reduce_ms.append(em.elapsed_time(e1))
+        stage_ms.append(eng.stage_millis())
         kern_ms.append(eng.kernel_ms())
-        reduce_keys(o)
+        reduce_host(winners_keys()[1])
     barrier()
     wall_s = time.perf_counter() - t_wall0
     launches = eng.launch_count() - launches0
@@ -235,11 +254,11 @@ def run_gpu(args):
         n_total = n_local
     ms_per_step = total_ms / args.steps
     value = n_total / (ms_per_step * 1e-3)
+    knife = eng.knife_edges()
 
     # ---- end-to-end arm (`e2e`): host buffers -> C-ABI -> host results, every step ----
     barrier()
     e2e_ms = []
-    h2d = d2h = 0
     for s in range(max(2, min(args.steps, 5)) + 1):
         t0 = time.perf_counter()
         eng._scene_key = None
@@ -247,8 +266,9 @@ def run_gpu(args):
         eng.prepare_plan(frame, models, plan)
         eng.search_upload(plan, idx)
         eng.search_run(sc)
-        o = eng.search_download(n_local)
-        reduce_keys(o)
+        eng.search_reduce()
+        wins, wkeys = winners_keys()   # device -> host read of the step's result (per-object winner records)
+        reduce_host(wkeys)
         torch.cuda.synchronize()
         if s:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
@@ -258,7 +278,7 @@ def run_gpu(args):
     h2d = (npix * 13 + len(plan.observed) * (24 + 24 + 8 + 4) + n_specs * 40
            + sum(m.mesh.vertices.size * 16 + m.mesh.triangles.size * 4 for m in models.values())
            + n_local * (96 + 12))
-    d2h = n_local * (96 + 96 + 4 * 6) + 8 * len(plan.active)
+    d2h = 8 * 28 * len(models) + 32
     e2e_t = float(np.median(e2e_ms)) * 1e-3
     if world > 1:
         t = torch.tensor([e2e_t], dtype=torch.float64, device=coll_dev)
@@ -266,30 +286,39 @@ def run_gpu(args):
         e2e_t = float(t.item())
     e2e_value = n_total / e2e_t
     # the user-facing call itself: estimate_poses(frame, models, cfg) = host planning (observed cloud,
-    # proposals, target specs) + everything above + result assembly; rank 0, single GPU only
-    api_ms = None
-    if world == 1:
-        import paper_2008_00326_b200.engine as E
-        from paper_2008_00326_b200 import estimate_poses
-        E._default = eng
-        ts = []
+    # proposals, target specs) + everything above + result assembly; at N>1 it is the distributed call
+    # (every rank returns the same SearchResult)
+    import paper_2008_00326_b200.engine as E
+    from paper_2008_00326_b200 import estimate_poses
+    E._default = eng
+    ts = []
+    if world == 1 or device_comm:
         for s_ in range(3):
+            barrier()
             t0 = time.perf_counter()
             res = estimate_poses(frame, models, cfg)
+            torch.cuda.synchronize()
             if s_:
                 ts.append((time.perf_counter() - t0) * 1e3)
-        api_ms = float(np.median(ts))
         assert res.proposals_evaluated == n_total
+    api_ms = float(np.median(ts)) if ts else None
+    if api_ms is not None and world > 1:
+        t = torch.tensor([api_ms], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        api_ms = float(t.item())
 
     if rank != 0:
+        if device_comm:
+            eng.lib.px_comm_destroy(eng.ctx)
         if world > 1:
             dist.destroy_process_group()
         return
 
     # ---- roofline of the dominant kernel (GICP refine) ----
+    eng.search_run(sc)  # the e2e / estimate_poses runs above replaced the resident shard's results
     full = eng.search_download(n_local)
-    ncs, cap0, cap1 = eng.search_stats(n_local)
-    ab = algorithmic_bytes(n_local, models, plan.flat_oid[idx], full, ncs, cap0, cap1, cfg.refine)
+    ncs, cap0, cap1, n_m, n_fp = eng.search_stats(n_local)
+    ab = algorithmic_bytes(n_local, models, plan.flat_oid[idx], full, ncs, cap0, cap1, cfg.refine, n_m, n_fp)
     st = {k: float(np.mean([s[k] for s in stage_ms])) for k in stage_ms[0]}
     # per kernel: mean over the timed steps of (total ms, launches) per step
     kern = {k: (float(np.mean([m[k][0] for m in kern_ms])), float(np.mean([m[k][1] for m in kern_ms]))) for k in kern_ms[0]}
@@ -341,15 +370,19 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload][0]} scene, mode={cfg.mode}, refine={cfg.refine}, "
-                               f"candidates/GPU={n_local}, total={n_total}, stride={cfg.stride}, 640x480",
-                   "candidates_per_step": n_total, "sharding": "grid cells round-robin across ranks; all_reduce(MIN) of packed (cost,pose-id) keys",
+        "config": {"workload": workload_string(args.workload, cfg),
+                   "candidates_per_step": n_total, "candidates_per_gpu": n_local,
+                   "sharding": "grid cells round-robin across ranks; ONE ncclAllReduce(MIN) of the packed (cost,pose-id) keys "
+                               "per step on libpx's own communicator, inside the timed region",
+                   "collective": ("nccl (px_search_reduce, device-side)" if device_comm else
+                                  ("none (single rank)" if world == 1 else f"{backend} through host memory (test knob)")),
                    "l2": "256 MiB flush between timed steps; per-step scratch also exceeds L2"},
-        "stage_ms": st, "wall_s_timed_region": wall_s,
+        "stage_ms": st, "reduce_ms": float(np.mean(reduce_ms)), "wall_s_timed_region": wall_s,
+        "knife_edges": knife,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_t * 1e3,
                 "path": "scene + models + GICP target specs + candidates from host buffers -> C-ABI (targets cropped on the "
-                        "device) -> results on the host",
+                        "device, argmin + winner records reduced on the device) -> per-object results on the host",
                 "estimate_poses_ms": api_ms,
                 "estimate_poses_value": (n_total / (api_ms * 1e-3)) if api_ms else None},
         "gpu_launches": int(launches),
@@ -357,6 +390,8 @@ def run_gpu(args):
         "mean_iterations": float(full.iterations.mean()), "mean_rendered_points": float(full.n_rendered.mean()),
     }
     print(json.dumps(line))
+    if device_comm:
+        eng.lib.px_comm_destroy(eng.ctx)
     if world > 1:
         dist.destroy_process_group()
 
@@ -420,8 +455,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload][0]} scene, mode={cfg.mode}, refine={cfg.refine}",
-                   "candidates_per_step": len(pick)},
+        "config": {"workload": workload_string(args.workload, cfg), "candidates_per_step": plan.n,
+                   "sampled_candidates_per_step": len(pick),
+                   "sampling": "the CPU arm scores a bounded sample of the step's candidates (whole grid cells spaced uniformly "
+                               "over the workspace) and reports per-candidate throughput"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -441,14 +478,36 @@ def main():
     ap.add_argument("--scale", type=int, default=1, help="refine the yaw/viewpoint axis: candidates x scale (C5 sweep)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        # `python bench.py --gpus N` on its own: become N ranks (one process per GPU) under torchrun
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        if os.environ.get("PX_BENCH_PRINT_SPAWN"):  # CPU test hook: show the launch line, do not run it
+            print(json.dumps(cmd))
+            return
+        raise SystemExit(subprocess.call(cmd))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "b200" and world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: running {world} rank(s)", file=sys.stderr)
+    if world > 1 and args.impl == "b200":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (rank / nranks) on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import __graft_entry__ as ge
 
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return  # the CPU arm is one process: the other ranks exit without work
+        ge.build(load_native=False)  # compiles everything, loads only the oracle: no libpx.so in this process
+        run_reference(args)
+        return
     if int(os.environ.get("LOCAL_RANK", "0")) == 0:
         ge.build()
-    if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_gpu(args)
+    run_gpu(args)
 
 
 if __name__ == "__main__":

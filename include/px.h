@@ -73,7 +73,8 @@ int px_ctx_create(int device, px_ctx** out);
 void px_ctx_destroy(px_ctx* ctx);
 const char* px_last_error(const px_ctx* ctx); /* ctx may be NULL: last creation error */
 /* Launch on a caller-provided cudaStream_t (e.g. torch's current stream); NULL
- * restores the context's own stream. */
+ * restores the context's own (non-blocking) stream.  The legacy default stream
+ * also has handle 0: name it by CUDA's sentinel cudaStreamLegacy, (void*)0x1. */
 int px_ctx_set_stream(px_ctx* ctx, void* cuda_stream);
 int px_ctx_sync(px_ctx* ctx);
 /* Upper bound in bytes for per-chunk candidate scratch (default 8 GiB). */
@@ -186,11 +187,45 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg);
 int px_search_download(px_ctx* ctx, double* refined_poses, double* reg_T, int32_t* iters, int32_t* flags,
                        int32_t* j_o, int32_t* j_r, int32_t* n_first, int32_t* n_final,
                        uint64_t* best_key_per_model, double stage_ms[4]);
+/* ---- multi-GPU: the worker fan-out of parallel.parallel_map (parallel.py:28-37) becomes one
+ * process per GPU, each scoring a shard of the candidates; the ordered gather + select_best
+ * (search.py:178-183, 346-372) becomes ONE NCCL all-reduce(MIN) of the packed per-object keys.
+ * NCCL is bound at run time (dlopen: `nccl_path`, else the libnccl.so.2 already mapped by torch,
+ * else the loader path), so libpx.so has no link-time dependency on it.
+ * px_comm_unique_id: rank 0 creates the 128-byte ncclUniqueId; the host broadcasts it to the other
+ * ranks (torch.distributed, MPI, a file ...); px_comm_init: every rank joins (ncclCommInitRank on
+ * the context's device). */
+int px_comm_unique_id(px_ctx* ctx /* nullable */, const char* nccl_path /* nullable */, uint8_t id[128]);
+int px_comm_init(px_ctx* ctx, const char* nccl_path /* nullable */, const uint8_t id[128], int32_t rank, int32_t world);
+int px_comm_destroy(px_ctx* ctx);
+int px_comm_info(const px_ctx* ctx, int32_t* rank, int32_t* world, int32_t* nccl_version);
+/* After px_search_run, enqueued on the context stream WITHOUT a host synchronisation (so that a CUDA
+ * event recorded after it covers the collective): all-reduce(MIN) of the per-model packed keys across
+ * the communicator (skipped when px_comm_init was not called), then the record of every model's
+ * winning candidate is extracted on the device and, across ranks, delivered to every rank by an
+ * all-reduce(MAX) over the records' raw 64-bit words (only the owning rank's record is non-zero).
+ * The keys px_search_download returns afterwards are the global ones. */
+int px_search_reduce(px_ctx* ctx);
+/* Per uploaded model, in upload order (any pointer may be NULL): global packed key (UINT64_MAX = no
+ * candidate), the winner's refined candidate pose (12) and applied GICP correction (12), its j_o, j_r,
+ * and the largest final-render point count over all ranks' candidates of that model
+ * (SearchResult.max_rendered_points, search.py:374-377).  Synchronises. */
+int px_search_winners(px_ctx* ctx, uint64_t* best_key, double* refined_pose, double* reg_T, int32_t* j_o,
+                      int32_t* j_r, int32_t* max_points);
+
 /* Work counters of the last px_search_run for roofline accounting (any pointer
  * may be NULL): per candidate, the sum over GICP iterations of the
- * correspondence count, and the stride-grid pixels inside the screen bounding
- * box of the first / final render (n_c, A_g). */
-int px_search_stats(px_ctx* ctx, int32_t* ncorr_sum, int64_t* cap_first, int64_t* cap_final);
+ * correspondence count, the stride-grid pixels inside the screen bounding
+ * box of the first / final render, the rendered points with an observed neighbour
+ * within delta and the observed points selected for the candidate (cost.py:121-152)
+ * (n_c, A_g, n_m, n_fp). */
+int px_search_stats(px_ctx* ctx, int32_t* ncorr_sum, int64_t* cap_first, int64_t* cap_final, int32_t* n_match,
+                    int32_t* n_footprint);
+/* Knife-edge log of the last px_search_run: margins[0] = min |d2 - delta^2| over every
+ * rendered point's nearest observed neighbour, margins[1] = min |dE00 - tau_c| over every colour-gated match
+ * (+inf when no such decision was taken).  The integer costs are exact reproductions of the reference's unless a
+ * decision sits within the floating-point disagreement of the two sides (~1e-12): these two numbers show it did not. */
+int px_search_knife_edges(px_ctx* ctx, double margins[2]);
 /* Per-kernel timing of the GICP stage (bench.py's roofline).  When switched on, px_search_run brackets
  * every launch of the refine stage with CUDA events on the context stream; px_search_kernel_ms then
  * returns, for the last run, total milliseconds and launch counts of

@@ -67,13 +67,20 @@ _SIGS = {
     "px_search_upload": (C.c_int, [vp, C.c_int64, i32p, f64p, i32p, i32p]),
     "px_search_run": (C.c_int, [vp, C.POINTER(SearchCfg)]),
     "px_search_download": (C.c_int, [vp, f64p, f64p, i32p, i32p, i32p, i32p, i32p, i32p, u64p, f64p]),
-    "px_search_stats": (C.c_int, [vp, i32p, i64p, i64p]),
+    "px_search_stats": (C.c_int, [vp, i32p, i64p, i64p, i32p, i32p]),
     "px_targets_build_capsules": (C.c_int, [vp, C.c_int32, f64p, f64p, C.POINTER(GicpCfg)]),
     "px_targets_build_labels": (C.c_int, [vp, C.c_int32, i32p, C.POINTER(GicpCfg)]),
     "px_targets_info": (C.c_int, [vp, i32p, i64p]),
     "px_targets_download": (C.c_int, [vp, i64p, f64p, i32p]),
     "px_ctx_set_kernel_timing": (C.c_int, [vp, C.c_int32]),
     "px_search_kernel_ms": (C.c_int, [vp, f64p, i64p]),
+    "px_comm_unique_id": (C.c_int, [vp, C.c_char_p, u8p]),
+    "px_comm_init": (C.c_int, [vp, C.c_char_p, u8p, C.c_int32, C.c_int32]),
+    "px_comm_destroy": (C.c_int, [vp]),
+    "px_comm_info": (C.c_int, [vp, i32p, i32p, i32p]),
+    "px_search_reduce": (C.c_int, [vp]),
+    "px_search_winners": (C.c_int, [vp, u64p, f64p, f64p, i32p, i32p, i32p]),
+    "px_search_knife_edges": (C.c_int, [vp, f64p]),
     "px_model_count": (C.c_int, [vp]),
     "px_model_ids": (C.c_int, [vp, i32p]),
 }

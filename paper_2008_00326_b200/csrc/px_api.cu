@@ -1,4 +1,6 @@
 // px_api.cu -- context, device memory and the C-ABI of libpx.so (include/px.h).
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -94,7 +96,7 @@ struct px_ctx {
   CloudStore clouds;
   DevBuf src_cov, w_buf, corr, nn, st_pose, st_i, st_hg, total_dev;
   long long refine_plane = 0;  // plane stride of the structure-of-arrays refine scratch
-  DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1;
+  DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1, r_nm, r_nfp;
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
   double stage_ms[4] = {0, 0, 0, 0};
@@ -104,6 +106,12 @@ struct px_ctx {
   int64_t kernel_n[5] = {0, 0, 0, 0, 0};
   int chunks = 0;
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // multi-GPU: this context's NCCL communicator (px_comm_init) and the per-object winner records
+  void* comm = nullptr;
+  int comm_rank = 0, comm_world = 1;
+  DevBuf r_win, r_knife;
+  bool win_valid = false;
+  int32_t tidx_max = -1;  // largest resident target index (validated against n_targets at run time)
 };
 
 namespace {
@@ -246,7 +254,7 @@ int ensure_bitmap(px_ctx* ctx) {
 
 int run_cost(px_ctx* ctx, const CloudStore& cs, const int32_t* slot_dev, const double* cyl_pose_dev, double delta,
              double tau_c, int use_color, int32_t* jo_dev, int32_t* jr_dev, const int32_t* rank_dev,
-             unsigned long long* key_dev, int lab_is_linear = 0) {
+             unsigned long long* key_dev, int lab_is_linear = 0, int32_t* nm_dev = nullptr, int32_t* nfp_dev = nullptr) {
   if (!ctx->organised) return fail(ctx, PX_E_ARG, "scene cloud is not the organised stride-grid cloud");
   if (int r = ensure_bitmap(ctx)) return r;
   CostArgs a{};
@@ -264,7 +272,8 @@ int run_cost(px_ctx* ctx, const CloudStore& cs, const int32_t* slot_dev, const d
   a.bitmap = ctx->bitmap.as<uint32_t>();
   a.bitmap_words = (ctx->cam.GW * ctx->cam.GH + 31) / 32 + 1;
   a.bitmap_slots = ctx->bitmap_slots;
-  a.j_o = jo_dev, a.j_r = jr_dev, a.rank = rank_dev, a.best_key = key_dev;
+  a.j_o = jo_dev, a.j_r = jr_dev, a.rank = rank_dev, a.best_key = key_dev, a.n_match = nm_dev, a.n_foot = nfp_dev;
+  a.knife = key_dev ? ctx->r_knife.as<unsigned long long>() : nullptr;  // fused search only
   CU(launch_cost(a, ctx->stream));
   ctx->launches += 1;
   return 0;
@@ -283,8 +292,8 @@ int check_gicp(px_ctx* ctx, const px_gicp_cfg& g) {
   if (g.k_covariance < 4 || g.k_covariance > PX_KCOV_MAX)
     return fail(ctx, PX_E_LIMIT, "k_covariance must lie in [4, " + std::to_string(PX_KCOV_MAX) + "]");
   if (g.max_iterations < 0) return fail(ctx, PX_E_ARG, "max_iterations < 0");
-  if (ctx->tgt_k != g.k_covariance || ctx->tgt_gate != g.max_correspondence_distance)
-    return fail(ctx, PX_E_ARG, "targets were uploaded with a different k_covariance / max_correspondence_distance");
+  if (ctx->tgt_k != g.k_covariance || ctx->tgt_gate != g.max_correspondence_distance || ctx->tgt_eps != g.epsilon)
+    return fail(ctx, PX_E_ARG, "targets were uploaded with a different k_covariance / epsilon / max_correspondence_distance");
   return 0;
 }
 
@@ -299,6 +308,46 @@ int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   CU(ctx->w_buf.ensure(sizeof(double) * 10 * tot));
   return 0;
 }
+
+// ---- NCCL, bound at run time (no link-time dependency: torch ships libnccl.so.2) ----------------
+struct px_nccl_id {
+  char internal[128];  // ncclUniqueId (NCCL_UNIQUE_ID_BYTES)
+};
+struct NcclApi {
+  void* handle = nullptr;
+  int (*GetUniqueId)(px_nccl_id*) = nullptr;
+  int (*CommInitRank)(void**, int, px_nccl_id, int) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  int (*GetVersion)(int*) = nullptr;
+} g_nccl;
+enum { PX_NCCL_UINT64 = 5, PX_NCCL_MAX = 2, PX_NCCL_MIN = 3 };  // ncclDataType_t / ncclRedOp_t values (nccl.h)
+
+int nccl_load(px_ctx* ctx, const char* path) {
+  if (g_nccl.handle) return 0;
+  void* h = nullptr;
+  if (path && *path) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the copy torch already mapped
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(ctx, PX_E_ARG, std::string("cannot load NCCL: ") + dlerror());
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.GetVersion = (decltype(g_nccl.GetVersion))dlsym(h, "ncclGetVersion");
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.CommDestroy || !g_nccl.AllReduce || !g_nccl.GetErrorString)
+    return fail(ctx, PX_E_ARG, "NCCL library lacks a required symbol");
+  g_nccl.handle = h;
+  return 0;
+}
+#define NC(call)                                                                                         \
+  do {                                                                                                   \
+    int r_ = (call);                                                                                     \
+    if (r_ != 0) return fail(ctx, PX_E_CUDA, std::string(#call) + ": " + g_nccl.GetErrorString(r_));     \
+  } while (0)
 
 }  // namespace
 
@@ -345,8 +394,11 @@ void px_ctx_destroy(px_ctx* ctx) {
                     &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->st_hg, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
-                    &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1};
+                    &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1, &ctx->r_nm, &ctx->r_nfp};
   for (DevBuf* b : bufs) b->release();
+  ctx->r_win.release(), ctx->r_knife.release();
+  if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  ctx->comm = nullptr;
   ctx->clouds.release();
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
@@ -361,6 +413,8 @@ const char* px_last_error(const px_ctx* ctx) { return ctx ? ctx->err.c_str() : g
 int px_ctx_set_stream(px_ctx* ctx, void* s) {
   if (!ctx) return PX_E_ARG;
   cudaStreamSynchronize(ctx->stream);
+  // NULL = the context's own non-blocking stream.  The legacy default stream has handle 0 as well, so it must be
+  // named by CUDA's own sentinel cudaStreamLegacy ((void*)0x1); cudaStreamPerThread is (void*)0x2.
   ctx->stream = s ? (cudaStream_t)s : ctx->own_stream;
   return 0;
 }
@@ -385,6 +439,8 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   if (!ctx) return PX_E_ARG;
   if (H <= 0 || W <= 0 || stride < 1 || !depth || !valid || !labels || !intr || n_obs < 0)
     return fail(ctx, PX_E_ARG, "px_scene_upload: bad arguments");
+  if ((W + stride - 1) / stride > PX_TILE_PIX)
+    return fail(ctx, PX_E_LIMIT, "image rows wider than " + std::to_string(PX_TILE_PIX) + " stride-grid pixels do not fit the z-buffer tile");
   CU(cudaSetDevice(ctx->device));
   Camera& c = ctx->cam;
   c.fx = intr[0], c.fy = intr[1], c.cx = intr[2], c.cy = intr[3];
@@ -607,6 +663,8 @@ int px_rasterize(px_ctx* ctx, int32_t object_id, const double pose[12], double* 
                  int32_t* owner) {
   if (!ctx || !pose || !zbuf || !cbuf || !valid || !owner) return fail(ctx, PX_E_ARG, "px_rasterize: bad arguments");
   if (!ctx->have_scene) return fail(ctx, PX_E_ARG, "no scene uploaded (camera comes from the scene)");
+  if (ctx->cam.W > PX_TILE_PIX)
+    return fail(ctx, PX_E_LIMIT, "image rows wider than " + std::to_string(PX_TILE_PIX) + " pixels do not fit the z-buffer tile");
   CU(cudaSetDevice(ctx->device));
   std::vector<int32_t> slots;
   if (int r = slots_from_ids(ctx, &object_id, 1, slots)) return r;
@@ -856,7 +914,7 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
       double m = 0.0;
       for (long long i = off[(size_t)t]; i < off[(size_t)t + 1]; ++i)
         for (int d = 0; d < 3; ++d) m = std::max(m, std::fabs(points[3 * i + d]));
-      orgs[(size_t)t].err = std::ldexp(1.5 * (2.0 * m + 1.0), -24);
+      orgs[(size_t)t].err = std::ldexp(1.5 * (2.0 * m + gate + 1.0), -24);  // queries that can match: |q| <= m + gate
     }
   }
   ctx->tgt_organised = org, ctx->tgt_obs_valid = false;
@@ -906,6 +964,7 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   a.obs_pts = ctx->obs_pts.as<double>(), a.obs_labels = ctx->obs_labels.as<int32_t>();
   a.obs_cell = ctx->obs_cell.as<int32_t>(), a.gidx = ctx->gidx.as<int32_t>(), a.n_obs = ctx->n_obs, a.GW = ctx->cam.GW;
   a.world = ctx->tgt_world.as<double>();
+  a.gate = cfg->max_correspondence_distance;
   a.cnt = ctx->tgt_sizes.as<long long>(), a.cells = a.cnt + n1, a.nodes = a.cells + n1;
   long long* off = ctx->tgt_off.as<long long>();
   long long* coff = ctx->tgt_scans.as<long long>();
@@ -1188,8 +1247,14 @@ int px_search_upload(px_ctx* ctx, int64_t n, const int32_t* object_ids, const do
   if (int r = h2d(ctx, ctx->c_pose, poses, (size_t)n * 96)) return r;
   if (int r = h2d(ctx, ctx->c_rank, rank, (size_t)n * 4)) return r;
   ctx->have_tidx = target_idx != nullptr;
-  if (target_idx)
+  ctx->tidx_max = -1;
+  if (target_idx) {
+    for (int64_t i = 0; i < n; ++i) {
+      if (target_idx[i] < 0) return fail(ctx, PX_E_ARG, "negative target index");
+      ctx->tidx_max = std::max(ctx->tidx_max, target_idx[i]);
+    }
     if (int r = h2d(ctx, ctx->c_tidx, target_idx, (size_t)n * 4)) return r;
+  }
   CU(cudaStreamSynchronize(ctx->stream));  // `slots` is stack-owned
   ctx->n_cand = n;
   return 0;
@@ -1260,7 +1325,7 @@ static int search_range(px_ctx* ctx, const px_search_cfg* cfg, int64_t lo, int64
   if (timed) CU(cudaEventRecord(ctx->ev[3], ctx->stream));
   if (int r = run_cost(ctx, ctx->clouds, slot, cfg->mode3dof ? cost_pose : nullptr, cfg->delta, cfg->tau_c, cfg->use_color,
                        ctx->r_jo.as<int32_t>() + lo, ctx->r_jr.as<int32_t>() + lo, ctx->c_rank.as<int32_t>() + lo,
-                       ctx->r_key.as<unsigned long long>(), 1))
+                       ctx->r_key.as<unsigned long long>(), 1, ctx->r_nm.as<int32_t>() + lo, ctx->r_nfp.as<int32_t>() + lo))
     return r;
   if (timed) CU(cudaEventRecord(ctx->ev[4], ctx->stream));
   // per-chunk stage times accumulate (a split run is a sequence of such chunks)
@@ -1288,12 +1353,16 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
   if (cfg->refine) {
     if (!ctx->have_tidx) return fail(ctx, PX_E_ARG, "refine requested but no target_idx uploaded");
     if (int r = check_gicp(ctx, cfg->gicp)) return r;
+    // the targets may have been replaced since px_search_upload (px_targets_*, px_refine_batch callers)
+    if (ctx->tidx_max >= ctx->n_targets)
+      return fail(ctx, PX_E_ARG, "resident candidates reference target " + std::to_string(ctx->tidx_max) + " but only " +
+                                     std::to_string(ctx->n_targets) + " targets are resident");
   }
   if (int r = sync_models(ctx)) return r;
   const size_t nn = (size_t)std::max<int64_t>(n, 1);
   CU(ctx->r_T.ensure(nn * 96));
   CU(ctx->r_pose.ensure(nn * 96));
-  DevBuf* ib[] = {&ctx->r_iters, &ctx->r_flags, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst, &ctx->r_nfinal, &ctx->r_ncorr};
+  DevBuf* ib[] = {&ctx->r_iters, &ctx->r_flags, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst, &ctx->r_nfinal, &ctx->r_ncorr, &ctx->r_nm, &ctx->r_nfp};
   for (DevBuf* b : ib) CU(b->ensure(nn * 4));
   CU(ctx->r_cap0.ensure(nn * 8));
   CU(ctx->r_cap1.ensure(nn * 8));
@@ -1302,6 +1371,11 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
   CU(cudaMemsetAsync(ctx->r_key.p, 0xff, sizeof(unsigned long long) * std::max<size_t>(ctx->models.size(), 1), ctx->stream));
   CU(cudaMemsetAsync(ctx->r_iters.p, 0, nn * 4, ctx->stream));
   CU(cudaMemsetAsync(ctx->r_flags.p, 0, nn * 4, ctx->stream));
+  {
+    CU(ctx->r_knife.ensure(16));
+    static const double inf2[2] = {INFINITY, INFINITY};
+    CU(cudaMemcpyAsync(ctx->r_knife.p, inf2, 16, cudaMemcpyHostToDevice, ctx->stream));
+  }
   if (!cfg->refine) {
     // identity corrections
     std::vector<double> I((size_t)n * 12, 0.0);
@@ -1311,6 +1385,7 @@ int px_search_run(px_ctx* ctx, const px_search_cfg* cfg) {
   }
   for (double& m : ctx->stage_ms) m = 0.0;
   for (int i = 0; i < 5; ++i) ctx->kernel_ms[i] = 0.0, ctx->kernel_n[i] = 0;
+  ctx->win_valid = false;
   if (n == 0) return 0;
   ctx->chunks = 0;
   if (int r = search_range(ctx, cfg, 0, n)) return r;
@@ -1352,10 +1427,111 @@ int px_search_kernel_ms(px_ctx* ctx, double ms[5], int64_t launches[5]) {
   return 0;
 }
 
-int px_search_stats(px_ctx* ctx, int32_t* ncorr_sum, int64_t* cap_first, int64_t* cap_final) {
+// ---- multi-GPU: the one collective ------------------------------------------------------------
+
+int px_comm_unique_id(px_ctx* ctx, const char* nccl_path, uint8_t id[128]) {
+  if (!id) return fail(ctx, PX_E_ARG, "px_comm_unique_id: id is NULL");
+  if (int r = nccl_load(ctx, nccl_path)) return r;
+  px_nccl_id u;
+  NC(g_nccl.GetUniqueId(&u));
+  memcpy(id, u.internal, sizeof u.internal);
+  return 0;
+}
+
+int px_comm_init(px_ctx* ctx, const char* nccl_path, const uint8_t id[128], int32_t rank, int32_t world) {
+  if (!ctx || !id || world < 1 || rank < 0 || rank >= world) return fail(ctx, PX_E_ARG, "px_comm_init: bad arguments");
+  if (int r = nccl_load(ctx, nccl_path)) return r;
+  CU(cudaSetDevice(ctx->device));
+  if (ctx->comm) g_nccl.CommDestroy(ctx->comm), ctx->comm = nullptr;
+  px_nccl_id u;
+  memcpy(u.internal, id, sizeof u.internal);
+  NC(g_nccl.CommInitRank(&ctx->comm, world, u, rank));
+  ctx->comm_rank = rank, ctx->comm_world = world;
+  return 0;
+}
+
+int px_comm_destroy(px_ctx* ctx) {
+  if (!ctx) return PX_E_ARG;
+  if (ctx->comm) {
+    cudaStreamSynchronize(ctx->stream);
+    g_nccl.CommDestroy(ctx->comm);
+  }
+  ctx->comm = nullptr, ctx->comm_rank = 0, ctx->comm_world = 1;
+  return 0;
+}
+
+int px_comm_info(const px_ctx* ctx, int32_t* rank, int32_t* world, int32_t* nccl_version) {
+  if (!ctx) return PX_E_ARG;
+  if (rank) *rank = ctx->comm_rank;
+  if (world) *world = ctx->comm ? ctx->comm_world : 1;
+  if (nccl_version) {
+    int v = 0;
+    if (g_nccl.GetVersion) g_nccl.GetVersion(&v);
+    *nccl_version = v;
+  }
+  return 0;
+}
+
+int px_search_reduce(px_ctx* ctx) {
+  if (!ctx) return PX_E_ARG;
+  CU(cudaSetDevice(ctx->device));
+  const size_t nm = std::max<size_t>(ctx->models.size(), 1);
+  unsigned long long* keys = ctx->r_key.as<unsigned long long>();
+  if (!keys) return fail(ctx, PX_E_ARG, "px_search_reduce: no search has run");
+  CU(ctx->r_win.ensure(nm * PX_WIN_WORDS * 8));
+  unsigned long long* win = ctx->r_win.as<unsigned long long>();
+  CU(cudaMemsetAsync(win, 0, nm * PX_WIN_WORDS * 8, ctx->stream));
+  if (ctx->comm) NC(g_nccl.AllReduce(keys, keys, nm, PX_NCCL_UINT64, PX_NCCL_MIN, ctx->comm, ctx->stream));
+  WinnerArgs a{};
+  a.n = (int)ctx->n_cand;
+  a.model_slot = ctx->c_slot.as<int32_t>(), a.rank = ctx->c_rank.as<int32_t>();
+  a.j_o = ctx->r_jo.as<int32_t>(), a.j_r = ctx->r_jr.as<int32_t>(), a.n_final = ctx->r_nfinal.as<int32_t>();
+  a.refined = ctx->r_pose.as<double>(), a.reg_T = ctx->r_T.as<double>();
+  a.best_key = keys, a.win = win;
+  CU(launch_winners(a, ctx->stream));
+  if (a.n) ctx->launches += 1;
+  if (ctx->comm) NC(g_nccl.AllReduce(win, win, nm * PX_WIN_WORDS, PX_NCCL_UINT64, PX_NCCL_MAX, ctx->comm, ctx->stream));
+  ctx->win_valid = true;
+  return 0;
+}
+
+int px_search_winners(px_ctx* ctx, uint64_t* best_key, double* refined, double* reg_T, int32_t* j_o, int32_t* j_r,
+                      int32_t* max_points) {
+  if (!ctx) return PX_E_ARG;
+  if (!ctx->win_valid) return fail(ctx, PX_E_ARG, "px_search_winners: call px_search_reduce after px_search_run first");
+  const size_t nm = ctx->models.size();
+  std::vector<unsigned long long> w(std::max<size_t>(nm, 1) * PX_WIN_WORDS);
+  if (int r = d2h(ctx, w.data(), ctx->r_win.p, w.size() * 8)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (size_t s = 0; s < nm; ++s) {
+    const unsigned long long* r = w.data() + s * PX_WIN_WORDS;
+    if (best_key) best_key[s] = r[0] ? r[0] - 1ull : UINT64_MAX;  // word 0 holds key + 1; 0 = no candidate anywhere
+    for (int q = 0; q < 12; ++q) {
+      if (refined) memcpy(&refined[12 * s + q], &r[1 + q], 8);
+      if (reg_T) memcpy(&reg_T[12 * s + q], &r[13 + q], 8);
+    }
+    if (j_o) j_o[s] = (int32_t)r[25];
+    if (j_r) j_r[s] = (int32_t)r[26];
+    if (max_points) max_points[s] = (int32_t)r[27];
+  }
+  return 0;
+}
+
+int px_search_knife_edges(px_ctx* ctx, double margins[2]) {
+  if (!ctx || !margins) return PX_E_ARG;
+  if (!ctx->r_knife.p) return fail(ctx, PX_E_ARG, "px_search_knife_edges: no search has run");
+  if (int r = d2h(ctx, margins, ctx->r_knife.p, 16)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int px_search_stats(px_ctx* ctx, int32_t* ncorr_sum, int64_t* cap_first, int64_t* cap_final, int32_t* n_match,
+                    int32_t* n_footprint) {
   if (!ctx) return PX_E_ARG;
   const size_t n = (size_t)ctx->n_cand;
   if (int r = d2h(ctx, ncorr_sum, ctx->r_ncorr.p, n * 4)) return r;
+  if (int r = d2h(ctx, n_match, ctx->r_nm.p, n * 4)) return r;
+  if (int r = d2h(ctx, n_footprint, ctx->r_nfp.p, n * 4)) return r;
   if (int r = d2h(ctx, cap_first, ctx->r_cap0.p, n * 8)) return r;
   if (int r = d2h(ctx, cap_final, ctx->r_cap1.p, n * 8)) return r;
   CU(cudaStreamSynchronize(ctx->stream));

@@ -58,18 +58,23 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
 
   // ---- pass 1: rendered points -> nearest observed, gates, explained bits ----
   int within = 0, color_fail = 0;
+  double knife_d = CUDART_INF, knife_c = CUDART_INF;  // how close any gate decision came to its threshold
   int e_lo_u = GW, e_hi_u = -1, e_lo_v = GH, e_hi_v = -1;  // bounds of set bits (grid units)
   for (int i = lane; i < n; i += 32) {
     const double qx = rp[3 * i], qy = rp[3 * i + 1], qz = rp[3 * i + 2];
-    if (!(qz > a.delta)) continue;  // cannot bound the window; no observed depth <= 0 exists
-    const double zr = qz - a.delta;
-    const double ru = cam.fx * a.delta * (1.0 + fabs(qx / qz)) / zr + 1e-6;
-    const double rv = cam.fy * a.delta * (1.0 + fabs(qy / qz)) / zr + 1e-6;
-    const double uq = cam.fx * qx / qz + cam.cx, vq = cam.fy * qy / qz + cam.cy;  // continuous pixel coords
-    // observed point at grid (gu,gv) sits at continuous pixel (gu*st+0.5, gv*st+0.5)
-    int gu0 = (int)ceil((uq - ru - 0.5) / st), gu1 = (int)floor((uq + ru - 0.5) / st);
-    int gv0 = (int)ceil((vq - rv - 0.5) / st), gv1 = (int)floor((vq + rv - 0.5) / st);
-    gu0 = max(gu0, 0), gv0 = max(gv0, 0), gu1 = min(gu1, GW - 1), gv1 = min(gv1, GH - 1);
+    int gu0 = 0, gv0 = 0, gu1 = GW - 1, gv1 = GH - 1;
+    if (qz > a.delta) {
+      const double zr = qz - a.delta;
+      const double ru = cam.fx * a.delta * (1.0 + fabs(qx / qz)) / zr + 1e-6;
+      const double rv = cam.fy * a.delta * (1.0 + fabs(qy / qz)) / zr + 1e-6;
+      const double uq = cam.fx * qx / qz + cam.cx, vq = cam.fy * qy / qz + cam.cy;  // continuous pixel coords
+      // observed point at grid (gu,gv) sits at continuous pixel (gu*st+0.5, gv*st+0.5); the clamps run in
+      // floating point so that huge windows cannot overflow the int conversion
+      const double u0 = ceil((uq - ru - 0.5) / st), u1 = floor((uq + ru - 0.5) / st);
+      const double v0 = ceil((vq - rv - 0.5) / st), v1 = floor((vq + rv - 0.5) / st);
+      gu0 = (int)fmin(fmax(u0, 0.0), (double)GW), gu1 = (int)fmax(fmin(u1, (double)(GW - 1)), -1.0);
+      gv0 = (int)fmin(fmax(v0, 0.0), (double)GH), gv1 = (int)fmax(fmin(v1, (double)(GH - 1)), -1.0);
+    }  // else: a point closer to the camera than delta has no bounded window -- the whole grid is scanned (exact)
     double best = CUDART_INF;
     int bg = -1;
     for (int gv = gv0; gv <= gv1; ++gv)
@@ -79,6 +84,7 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
         const double d2 = dx * dx + dy * dy + dz * dz;  // NaN where the grid has no point
         if (d2 < best) best = d2, bg = g;
       }
+    if (bg >= 0) knife_d = fmin(knife_d, fabs(best - a.delta2));
     if (bg < 0 || !(best <= a.delta2)) continue;
     ++within;
     const int j = a.gidx[bg];
@@ -87,7 +93,9 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
       double L = rl[3 * i], A = rl[3 * i + 1], B = rl[3 * i + 2];
       if (a.lab_is_linear)  // raster.py:278 evaluated only for the points that reach the colour gate
         srgb_to_lab(srgb_encode1(L), srgb_encode1(A), srgb_encode1(B), L, A, B);
-      if (!(ciede2000(L, A, B, ol[0], ol[1], ol[2]) <= a.tau_c)) {
+      const double de = ciede2000(L, A, B, ol[0], ol[1], ol[2]);
+      knife_c = fmin(knife_c, fabs(de - a.tau_c));
+      if (!(de <= a.tau_c)) {
         ++color_fail;
         continue;
       }
@@ -98,13 +106,24 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
   }
   within = warp_sum(within);
   color_fail = warp_sum(color_fail);
+  if (a.knife) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      knife_d = fmin(knife_d, __shfl_xor_sync(0xffffffffu, knife_d, o));
+      knife_c = fmin(knife_c, __shfl_xor_sync(0xffffffffu, knife_c, o));
+    }
+    if (lane == 0) {  // non-negative doubles order like their bit patterns
+      if (knife_d < bits_d(*(volatile unsigned long long*)&a.knife[0])) atomicMin(&a.knife[0], dbits(knife_d));
+      if (knife_c < bits_d(*(volatile unsigned long long*)&a.knife[1])) atomicMin(&a.knife[1], dbits(knife_c));
+    }
+  }
   e_lo_u = warp_min(e_lo_u), e_lo_v = warp_min(e_lo_v), e_hi_u = warp_max(e_hi_u), e_hi_v = warp_max(e_hi_v);
   const int j_r = n - within + color_fail;
   __threadfence();
   __syncwarp();
 
   // ---- pass 2: observed points selected for this candidate ----
-  int j_o = 0;
+  int j_o = 0, n_foot = 0;
   if (a.cyl_poses) {
     const double* P = a.cyl_poses + 12 * (size_t)c;
     double p[12];
@@ -148,9 +167,11 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
       const double y = dot_f012(ox, oy, oz, p[1], p[5], p[9]) + ti1;
       const double z = dot_f012(ox, oy, oz, p[2], p[6], p[10]) + ti2;
       const bool sel = (x * x + y * y <= m.cyl_r2) && z >= m.cyl_zmin && z <= m.cyl_zmax;  // false on NaN
+      n_foot += sel;
       if (sel && !((__ldcg(&bm[g >> 5]) >> (g & 31)) & 1u)) ++j_o;
     }
     j_o = warp_sum(j_o);
+    n_foot = warp_sum(n_foot);
   } else {
     // label mode: j_o = count(label == oid) - count(label == oid & explained)
     int hit = 0;
@@ -165,6 +186,7 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
       }
     }
     j_o = a.label_count[slot] - warp_sum(hit);
+    n_foot = a.label_count[slot];
   }
   __syncwarp();
   // ---- clear the bits we set (bitmap is clean on entry and exit) ----
@@ -178,6 +200,8 @@ __global__ void __launch_bounds__(PX_COST_WARPS * 32) cost_kernel(CostArgs a) {
   if (lane == 0) {
     a.j_o[c] = j_o;
     a.j_r[c] = j_r;
+    if (a.n_match) a.n_match[c] = within;
+    if (a.n_foot) a.n_foot[c] = n_foot;
     if (a.best_key) {
       const unsigned long long key = ((unsigned long long)(unsigned)(j_o + j_r) << 32) | (unsigned)a.rank[c];
       atomicMin(&a.best_key[slot], key);
@@ -192,6 +216,31 @@ cudaError_t launch_cost(const CostArgs& a, cudaStream_t st) {
   int blocks = (a.ren.n + PX_COST_WARPS - 1) / PX_COST_WARPS;
   if (blocks > a.bitmap_slots / PX_COST_WARPS) blocks = a.bitmap_slots / PX_COST_WARPS;
   cost_kernel<<<blocks, PX_COST_WARPS * 32, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// search.py:346-372 on the device: the record of every object's winning candidate (see WinnerArgs)
+__global__ void __launch_bounds__(256) winner_kernel(WinnerArgs a) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.n) return;
+  const int slot = a.model_slot[c];
+  unsigned long long* w = a.win + (size_t)slot * PX_WIN_WORDS;
+  const unsigned long long nf = (unsigned long long)(unsigned)a.n_final[c];
+  if (nf > *(volatile unsigned long long*)&w[27]) atomicMax(&w[27], nf);  // racy read = filter only
+  const unsigned long long key = ((unsigned long long)(unsigned)(a.j_o[c] + a.j_r[c]) << 32) | (unsigned)a.rank[c];
+  if (key != a.best_key[slot]) return;
+  w[0] = key + 1ull;  // 0 = no candidate anywhere
+  for (int q = 0; q < 12; ++q) {
+    w[1 + q] = dbits(a.refined[12 * (size_t)c + q]);
+    w[13 + q] = dbits(a.reg_T[12 * (size_t)c + q]);
+  }
+  w[25] = (unsigned long long)(unsigned)a.j_o[c];
+  w[26] = (unsigned long long)(unsigned)a.j_r[c];
+}
+
+cudaError_t launch_winners(const WinnerArgs& a, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  winner_kernel<<<(a.n + 255) / 256, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

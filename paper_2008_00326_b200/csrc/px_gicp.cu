@@ -360,6 +360,7 @@ __device__ unsigned long long g_nn_rhist[8];
 __device__ double g_nn_rayk;
 __device__ float* g_nn_prevq;
 __device__ unsigned long long g_nn_mhist[8];  // queries, with-prev, sb tests, blk tests, leaf pts, found, leaves opened
+__device__ unsigned long long g_nn_lhist[32];  // leaves opened per query: [seeded?][found?][bucket 0,1,2,3-4,5-8,9-16,17-32,33+]
 #define NN_STAT(i, v) atomicAdd(&g_nn_stats[i], (unsigned long long)(v))
 #else
 #define NN_STAT(i, v)
@@ -420,6 +421,9 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
       if (d2 <= best) best = d2, bj = prev;
     }
     float thr = nn_threshold(best, o.err);
+#ifdef PX_NN_STATS
+    int n_leaves_ = 0, n_improved_ = 0;
+#endif
     const float qxf = (float)qx, qyf = (float)qy, qzf = (float)qz;
     const int32_t* lstart = T.leaf_start + o.box_off + ti;  // (bw*bh + 1) entries per target
     const float4* lp = T.leaf32 + toff;                     // points grouped by block: {x, y, z, index bits}
@@ -476,11 +480,20 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
             if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;
           }
           if (improved) thr = nn_threshold(best, o.err);
+#ifdef PX_NN_STATS
+          ++n_leaves_, n_improved_ += improved;
+#endif
         }
       }
     if (bj == 0x7fffffff) best = CUDART_INF, bj = -1;
     NN_STAT(5, bj >= 0);
 #ifdef PX_NN_STATS
+    NN_STAT(7, n_improved_);
+    {
+      const int L = n_leaves_;
+      const int b_ = L == 0 ? 0 : L == 1 ? 1 : L == 2 ? 2 : L <= 4 ? 3 : L <= 8 ? 4 : L <= 16 ? 5 : L <= 32 ? 6 : 7;
+      atomicAdd(&g_nn_lhist[(prev >= 0 ? 16 : 0) + (bj >= 0 ? 8 : 0) + b_], 1ull);
+    }
     {
       int b_ = 7;
       if (bj >= 0) {
@@ -1216,10 +1229,19 @@ void dump_nn_stats() {
   unsigned long long h[8];
   cudaMemcpyFromSymbol(h, g_nn_stats, sizeof h);
   if (h[0])
-    fprintf(stderr, "[nn stats] queries %llu, with prev %.3f, found %.3f; per query: sb tests %.2f, blk tests %.2f, leaves %.2f, leaf pts %.2f\n",
-            h[0], (double)h[1] / h[0], (double)h[5] / h[0], (double)h[2] / h[0], (double)h[3] / h[0], (double)h[6] / h[0], (double)h[4] / h[0]);
+    fprintf(stderr, "[nn stats] queries %llu, with prev %.3f, found %.3f; per query: sb tests %.2f, blk tests %.2f, leaves %.2f (improving %.2f), leaf pts %.2f\n",
+            h[0], (double)h[1] / h[0], (double)h[5] / h[0], (double)h[2] / h[0], (double)h[3] / h[0], (double)h[6] / h[0], (double)h[7] / h[0], (double)h[4] / h[0]);
   cudaMemcpyFromSymbol(h, g_nn_rhist, sizeof h);
   fprintf(stderr, "[nn R hist] <0.5 %llu <1.5 %llu <2.5 %llu <3.5 %llu <5.5 %llu <8.5 %llu >=8.5 %llu notfound %llu\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
+  {
+    unsigned long long l[32];
+    cudaMemcpyFromSymbol(l, g_nn_lhist, sizeof l);
+    for (int g = 0; g < 4; ++g)
+      fprintf(stderr, "[nn leaves/query seeded=%d found=%d] 0:%llu 1:%llu 2:%llu 3-4:%llu 5-8:%llu 9-16:%llu 17-32:%llu 33+:%llu\n", g >> 1, g & 1,
+              l[8 * g], l[8 * g + 1], l[8 * g + 2], l[8 * g + 3], l[8 * g + 4], l[8 * g + 5], l[8 * g + 6], l[8 * g + 7]);
+    memset(l, 0, sizeof l);
+    cudaMemcpyToSymbol(g_nn_lhist, l, sizeof l);
+  }
   cudaMemcpyFromSymbol(h, g_nn_mhist, sizeof h);
   fprintf(stderr, "[nn motion mm] <.03 %llu <.1 %llu <.3 %llu <1 %llu <3 %llu <10 %llu >=10 %llu\n", h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
   memset(h, 0, sizeof h);

@@ -120,6 +120,7 @@ struct TgtBuildArgs {
   const double* params;       // mode 0: (n,5) cell x, cell y, z_lo, z_hi, radius (world frame)
   const int32_t* label_ids;   // mode 1: (n) object ids
   double c2w[12];             // camera -> world (mode 0)
+  double gate;                // max_correspondence_distance (enters the fp32 pruning error bound)
   // scene
   const double* obs_pts;      // (n_obs,3) camera frame
   const int32_t* obs_labels;  // (n_obs)
@@ -225,11 +226,32 @@ struct CostArgs {
   int bitmap_slots;            // number of warp slots the bitmap scratch holds (multiple of PX_COST_WARPS)
   int32_t* j_o;                // (n) out
   int32_t* j_r;                // (n) out
+  int32_t* n_match;            // (n) out, nullable: rendered points with an observed neighbour within delta (SURVEY 8(d) n_m)
+  int32_t* n_foot;             // (n) out, nullable: observed points selected for the candidate (n_fp)
+  unsigned long long* knife;   // nullable: [0] min |d2 - delta^2| over all gated neighbours, [1] min |dE - tau_c| (double bits)
   // fused argmin (search.py:178-183): key = total<<32 | rank
   const int32_t* rank;         // (n) rank of the candidate inside its object, nullable
   unsigned long long* best_key;  // per model slot, nullable
 };
 cudaError_t launch_cost(const CostArgs& a, cudaStream_t st);
+
+// Per-object winner records after the (all-reduced) argmin keys are known (search.py:346-372): the candidate whose
+// packed key equals best_key[slot] writes its record; every other record stays zero, so an all-reduce(MAX) over the
+// raw 64-bit words across ranks delivers the owner's bits unchanged.
+#define PX_WIN_WORDS 28  // key + 1 | refined pose (12) | applied correction (12) | j_o | j_r | max points in the final render
+struct WinnerArgs {
+  int n;
+  const int32_t* model_slot;          // (n)
+  const int32_t* rank;                // (n) rank in object
+  const int32_t* j_o;
+  const int32_t* j_r;
+  const int32_t* n_final;             // (n) points in the final render
+  const double* refined;              // (n,12)
+  const double* reg_T;                // (n,12)
+  const unsigned long long* best_key; // per model slot (global after the reduction)
+  unsigned long long* win;            // (n_models, PX_WIN_WORDS), zero on entry
+};
+cudaError_t launch_winners(const WinnerArgs& a, cudaStream_t st);
 
 struct KnnArgs {  // exact brute-force kNN, k <= PX_KCOV_MAX (neighbors.py:104-134)
   const double* q;

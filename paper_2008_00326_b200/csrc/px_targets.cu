@@ -126,7 +126,9 @@ __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int q = 1; q < 8; ++q) m = fmax(m, wmax[q]);
-    a.org[t].err = ldexp(1.5 * (2.0 * m + 1.0), -24);  // px_targets_upload: bound on the fp32 pruning errors
+    // px_targets_upload: bound on the fp32 pruning errors; a query that can still match lies within `gate` of a
+    // target point, so its coordinates are bounded by m + gate
+    a.org[t].err = ldexp(1.5 * (2.0 * m + a.gate + 1.0), -24);
   }
 }
 

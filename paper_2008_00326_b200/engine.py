@@ -369,12 +369,101 @@ class Engine:
         out.best_keys = {int(i): int(k) for i, k in zip(ids[:nm], keys[:nm])}
         return out
 
+    # -- multi-GPU (include/px.h: px_comm_*, px_search_reduce) ---------------------------
+    @staticmethod
+    def nccl_library() -> bytes | None:
+        """Path of the NCCL shared library torch ships (site-packages/nvidia/nccl/lib), or None to let
+        libpx pick the copy already mapped into the process / the loader path."""
+        import importlib.util
+        import os
+
+        env = os.environ.get("PX_NCCL_LIB")
+        if env:
+            return env.encode()
+        try:
+            spec = importlib.util.find_spec("nvidia.nccl")
+        except (ImportError, ValueError):
+            spec = None
+        for base in (list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []):
+            cand = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                return cand.encode()
+        return None
+
+    def comm_init(self, rank: int, world: int, unique_id: np.ndarray):
+        uid = np.ascontiguousarray(unique_id, dtype=np.uint8)
+        assert uid.shape == (128,)
+        rc = self.lib.px_comm_init(self.ctx, self.nccl_library(), N.ptr(uid, N.u8p), int(rank), int(world))
+        N.check(self.ctx, rc, "px_comm_init")
+
+    def comm_unique_id(self) -> np.ndarray:
+        uid = np.zeros(128, dtype=np.uint8)
+        N.check(self.ctx, self.lib.px_comm_unique_id(self.ctx, self.nccl_library(), N.ptr(uid, N.u8p)), "px_comm_unique_id")
+        return uid
+
+    def comm_init_torch(self):
+        """Join the ranks of the initialised torch.distributed group in libpx's own NCCL communicator: rank 0
+        creates the unique id, torch.distributed (the plumbing) broadcasts it, every rank calls px_comm_init."""
+        import torch
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        uid = self.comm_unique_id() if rank == 0 else np.zeros(128, dtype=np.uint8)
+        t = torch.from_numpy(uid)
+        if dist.get_backend() == "nccl":
+            t = t.to(torch.device("cuda", self.device))
+        dist.broadcast(t, src=0)
+        self.comm_init(rank, world, t.cpu().numpy())
+
+    def comm_world(self) -> int:
+        r, w, v = C.c_int32(0), C.c_int32(1), C.c_int32(0)
+        N.check(self.ctx, self.lib.px_comm_info(self.ctx, C.byref(r), C.byref(w), C.byref(v)), "px_comm_info")
+        return int(w.value)
+
+    def nccl_version(self) -> int:
+        r, w, v = C.c_int32(0), C.c_int32(1), C.c_int32(0)
+        N.check(self.ctx, self.lib.px_comm_info(self.ctx, C.byref(r), C.byref(w), C.byref(v)), "px_comm_info")
+        return int(v.value)
+
+    def search_reduce(self):
+        """Enqueue the argmin all-reduce + winner extraction behind the last search_run (no host sync)."""
+        N.check(self.ctx, self.lib.px_search_reduce(self.ctx), "px_search_reduce")
+
+    def search_winners(self) -> dict:
+        """{object_id: (key, refined (3,4), reg_T (3,4), j_o, j_r, max_points)} for every model with a
+        candidate on any rank."""
+        nm = int(self.lib.px_model_count(self.ctx))
+        keys = np.zeros(max(nm, 1), dtype=np.uint64)
+        ref, reg = np.zeros((max(nm, 1), 3, 4)), np.zeros((max(nm, 1), 3, 4))
+        jo, jr, mp = (np.zeros(max(nm, 1), dtype=np.int32) for _ in range(3))
+        rc = self.lib.px_search_winners(self.ctx, N.ptr(keys, N.u64p), N.ptr(ref, N.f64p), N.ptr(reg, N.f64p),
+                                        N.ptr(jo, N.i32p), N.ptr(jr, N.i32p), N.ptr(mp, N.i32p))
+        N.check(self.ctx, rc, "px_search_winners")
+        ids = np.zeros(max(nm, 1), dtype=np.int32)
+        self.lib.px_model_ids(self.ctx, N.ptr(ids, N.i32p))
+        no_key = np.uint64(0xFFFFFFFFFFFFFFFF)
+        return {int(ids[s]): (int(keys[s]), ref[s].copy(), reg[s].copy(), int(jo[s]), int(jr[s]), int(mp[s]))
+                for s in range(nm) if keys[s] != no_key}
+
+    def stage_millis(self) -> dict:
+        ms = np.zeros(4)
+        rc = self.lib.px_search_download(self.ctx, None, None, None, None, None, None, None, None, None, N.ptr(ms, N.f64p))
+        N.check(self.ctx, rc, "px_search_download")
+        return dict(zip(("render", "refine", "rerender", "cost"), (float(x) for x in ms)))
+
+    def knife_edges(self) -> dict:
+        """How close any gate decision of the last search came to its threshold."""
+        m = np.zeros(2)
+        N.check(self.ctx, self.lib.px_search_knife_edges(self.ctx, N.ptr(m, N.f64p)), "px_search_knife_edges")
+        return {"min_abs_d2_minus_delta2": float(m[0]), "min_abs_dE_minus_tau_c": float(m[1])}
+
     def search_stats(self, n):
-        nc = np.zeros(n, dtype=np.int32)
+        nc, nm, nfp = (np.zeros(n, dtype=np.int32) for _ in range(3))
         c0, c1 = np.zeros(n, dtype=np.int64), np.zeros(n, dtype=np.int64)
-        rc = self.lib.px_search_stats(self.ctx, N.ptr(nc, N.i32p), N.ptr(c0, N.i64p), N.ptr(c1, N.i64p))
+        rc = self.lib.px_search_stats(self.ctx, N.ptr(nc, N.i32p), N.ptr(c0, N.i64p), N.ptr(c1, N.i64p),
+                                      N.ptr(nm, N.i32p), N.ptr(nfp, N.i32p))
         N.check(self.ctx, rc, "px_search_stats")
-        return nc, c0, c1
+        return nc, c0, c1, nm, nfp
 
     KERNELS = ("gicp_init_kernel", "gicp_nn_kernel", "gicp_lin_kernel", "gicp_halve_kernel", "gicp_finish_kernel")
 

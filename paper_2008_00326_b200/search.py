@@ -210,6 +210,7 @@ class SearchPlan:
     w2c: np.ndarray | None = None
     c2w_vec_order: int = 0           # 0: rotation C-contiguous, 1: transposed view
     w2c_vec_order: int = 1
+    cam_to_world: RigidTransform | None = None  # the frame's own object (its array layout decides numpy's rounding order)
 
     @property
     def n(self) -> int:
@@ -308,7 +309,8 @@ def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = Tr
                       c2w=np.ascontiguousarray(cam_to_world.matrix3x4()),
                       w2c=np.ascontiguousarray(world_to_cam.matrix3x4()),
                       c2w_vec_order=_vec_order(cam_to_world.rotation),
-                      w2c_vec_order=_vec_order(world_to_cam.rotation))
+                      w2c_vec_order=_vec_order(world_to_cam.rotation),
+                      cam_to_world=cam_to_world)
     if cfg.refine and build_targets and plan.n:
         _plan_targets(plan, models, cam_to_world, materialise_targets)
     return plan
@@ -404,7 +406,9 @@ def _winner_rows(plan: SearchPlan, out: StageOutputs, index=None) -> dict:
 def _assemble(plan: SearchPlan, winners: dict, stage_millis: dict, t_start: float, max_pts: int) -> SearchResult:
     """Result records from the per-object winners (search.py:346-377)."""
     per_stage_total = sum(stage_millis.values())
-    c2w = RigidTransform.from_matrix3x4(plan.c2w)
+    # compose with the frame's own transform object: a transposed-view rotation rounds differently in numpy
+    # than a contiguous copy would (search.py:363 uses k.camera_pose as it is)
+    c2w = plan.cam_to_world if plan.cam_to_world is not None else RigidTransform.from_matrix3x4(plan.c2w)
     estimates = []
     for oid in plan.object_ids:
         if oid in plan.failures or oid not in plan.active or oid not in winners:
@@ -473,12 +477,24 @@ def estimate_poses_distributed(frame, models: dict, cfg: SearchConfig, runner=No
     if plan.n == 0:
         return _assemble(plan, {}, stage_millis, t_start, 0)
     idx = pxd.shard_index(plan, rank, world)
+    if device_run and dist.get_backend() == "nccl":
+        # the collective runs on the device: libpx's own NCCL communicator reduces the packed keys and
+        # delivers the winners' records to every rank (px_search_reduce); nothing per-candidate leaves the GPU
+        eng = default_engine()
+        if eng.comm_world() != world:
+            eng.comm_init_torch()
+        winners, stage_millis, max_pts = _device_search(eng, frame, models, plan, idx)
+        t = torch.tensor([stage_millis[k] for k in ("render", "refine", "rerender", "cost")], dtype=torch.float64,
+                         device=torch.device("cuda", eng.device))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # stage times: slowest rank
+        stage_millis = dict(zip(("render", "refine", "rerender", "cost"), (float(x) for x in t.cpu().numpy())))
+        return _assemble(plan, winners, stage_millis, t_start, max_pts)
     out = runner(frame, models, plan, idx)
     if out.stage_millis:
         stage_millis.update(out.stage_millis)
     mine = _winner_rows(plan, out, idx)
     keys = np.array([mine[o][0] if o in mine else pxd.NO_KEY for o in plan.active], dtype=np.int64)
-    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else None
+    dev = None  # host path (gloo / injected runner); the nccl path returned above
     best = pxd.allreduce_min(keys, dev)
     # payload of the winners: only the owning rank contributes non-zeros (keys are unique per candidate)
     pay = np.zeros((len(plan.active), 27))
@@ -503,6 +519,19 @@ def estimate_poses_distributed(frame, models: dict, cfg: SearchConfig, runner=No
     return _assemble(plan, winners, stage_millis, t_start, int(mp_h[0]))
 
 
+def _device_search(eng, frame, models, plan: SearchPlan, index=None):
+    """Upload, fused search, on-device argmin (+ NCCL reduction when a communicator is up); only the
+    per-object winner records come back to the host.  -> (winners, stage_millis, max_rendered_points)."""
+    eng.prepare_plan(frame, models, plan)
+    eng.search_upload(plan, index)
+    eng.search_run(eng.search_cfg(plan))
+    eng.search_reduce()
+    win = eng.search_winners()
+    winners = {o: win[o][:5] for o in plan.active if o in win}
+    max_pts = max([win[o][5] for o in plan.active if o in win], default=0)
+    return winners, eng.stage_millis(), max_pts
+
+
 def estimate_poses(frame, models: dict, cfg: SearchConfig) -> SearchResult:
     """Estimate a pose for every detected object (search.py:217-377)."""
     from .engine import default_engine
@@ -519,8 +548,13 @@ def estimate_poses(frame, models: dict, cfg: SearchConfig) -> SearchResult:
         out = StageOutputs(np.zeros((0, 3, 4)), np.zeros((0, 3, 4)), np.zeros(0, np.int32),
                            np.zeros(0, np.int32))
         return assemble_result(plan, out, t_start)
-    out = default_engine().run_plan(frame, models, plan)
-    return assemble_result(plan, out, t_start)
+    if cfg.trace_path:  # the per-candidate trace needs every candidate's costs on the host
+        out = default_engine().run_plan(frame, models, plan)
+        return assemble_result(plan, out, t_start)
+    winners, stage_millis, max_pts = _device_search(default_engine(), frame, models, plan)
+    sm = {"render": 0.0, "refine": 0.0, "rerender": 0.0, "cost": 0.0}
+    sm.update(stage_millis)
+    return _assemble(plan, winners, sm, t_start, max_pts)
 
 
 def result_to_json(result: SearchResult) -> str:
