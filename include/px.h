@@ -152,6 +152,20 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
                     const px_gicp_cfg* cfg, double* out_T, int32_t* out_iters, int32_t* out_flags,
                     double* out_residual, double* out_trace, int32_t* out_ntrace);
 
+/* Test export of registration._gicp_linearize (registration.py:233-338) for ONE source / target pair at the
+ * transform T, evaluated by the production kernels (source / target covariances as in registration.py:109-216, exact
+ * nearest neighbours :251-261, per-point W = (Cb + R Ca R^T)^-1 and the sums in source-index order :262-338).  Outputs
+ * (any may be NULL): H (36), g (6), f0, number of correspondences, corr (n) (target index or -1) and W (n,9) (zero rows
+ * where no weight was formed).  Replaces the resident targets. */
+int px_gicp_linearize(px_ctx* ctx, const double* src, int64_t n, const double* tgt, int64_t m, const double T[12],
+                      const px_gicp_cfg* cfg, double* h36, double* g6, double* f0, int32_t* n_corr, int64_t* corr,
+                      double* w);
+/* Test exports of the device colour functions: colorspace.ciede2000 (colorspace.py:58-124) for n Lab pairs, and
+ * colorspace.srgb_to_lab (:41-55) for n colours (linear_input != 0: linear-light input, encoded first as
+ * raster.py:278 does). */
+int px_ciede2000(px_ctx* ctx, const double* lab_a, const double* lab_b, int64_t n, double* out);
+int px_srgb_to_lab(px_ctx* ctx, const double* rgb, int64_t n, int32_t linear_input, double* lab_out);
+
 /* ---- cost (cost.py:91-162, search.py:189-202) -------------------------------- */
 /* Per-candidate (j_o, j_r) against the uploaded organised scene.  cyl_poses
  * (n,12) = camera-frame object pose per candidate for the inscribed-cylinder

@@ -60,6 +60,10 @@ _SIGS = {
     "px_targets_covariances": (C.c_int, [vp, f64p]),
     "px_refine_batch": (C.c_int, [vp, vp, i32p, f64p, C.POINTER(GicpCfg), f64p, i32p, i32p, f64p,
                                   f64p, i32p]),
+    "px_gicp_linearize": (C.c_int, [vp, f64p, C.c_int64, f64p, C.c_int64, f64p, C.POINTER(GicpCfg), f64p, f64p, f64p,
+                                    i32p, i64p, f64p]),
+    "px_ciede2000": (C.c_int, [vp, f64p, f64p, C.c_int64, f64p]),
+    "px_srgb_to_lab": (C.c_int, [vp, f64p, C.c_int64, C.c_int32, f64p]),
     "px_cost_batch": (C.c_int, [vp, vp, i32p, f64p, C.c_double, C.c_double, C.c_int32, i32p, i32p]),
     "px_rendered_cost": (C.c_int, [vp, f64p, f64p, C.c_int64, f64p, f64p, C.c_int64, C.c_double,
                                    C.c_double, C.c_int32, i32p, u8p]),

@@ -1130,6 +1130,128 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
   return rc;
 }
 
+// Test export: registration._gicp_linearize (registration.py:233-338) at the transform T for ONE source / target
+// pair, through the production kernels (gicp_init_kernel covariances, gicp_nn_kernel, gicp_lin_kernel's ordered
+// 43-lane sums).  Replaces the resident targets.
+int px_gicp_linearize(px_ctx* ctx, const double* src, int64_t n, const double* tgt, int64_t m, const double T[12],
+                      const px_gicp_cfg* cfg, double* h36, double* g6, double* f0, int32_t* n_corr, int64_t* corr,
+                      double* w) {
+  if (!ctx || !src || !tgt || !T || !cfg || n <= 0 || m <= 0) return fail(ctx, PX_E_ARG, "px_gicp_linearize: bad arguments");
+  if (n <= cfg->k_covariance || m <= cfg->k_covariance) return fail(ctx, PX_E_ARG, "px_gicp_linearize: need more than k points");
+  const int64_t offs[2] = {0, m};
+  if (int r = px_targets_upload(ctx, 1, offs, tgt, nullptr, cfg)) return r;
+  px_clouds* cl = nullptr;
+  const int32_t cnt = (int32_t)n;
+  if (int r = px_clouds_upload(ctx, 1, &cnt, src, nullptr, nullptr, &cl)) return r;
+  int rc = 0;
+  DevBuf dti, dinit, dT, dit, dfl;
+  do {
+    if ((rc = ensure_refine_scratch(ctx, cl->s.total_cap, 1))) break;
+    const int32_t ti = 0;
+    if ((rc = h2d(ctx, dti, &ti, 4)) || (rc = h2d(ctx, dinit, T, 96))) break;
+    cudaError_t e;
+    if ((e = dT.ensure(96)) || (e = dit.ensure(4)) || (e = dfl.ensure(4))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    RefineArgs a{};
+    a.src = clouds_dev(cl->s);
+    a.tgt = targets_dev(ctx);
+    a.target_idx = dti.as<int32_t>(), a.init_T = dinit.as<double>();
+    a.cfg = gicp_dev(*cfg);
+    a.cfg.max_iter = std::max(a.cfg.max_iter, 1);
+    a.cam = ctx->cam;
+    a.src_soa = ctx->src_cov.as<double>(), a.w_buf = ctx->w_buf.as<double>(), a.plane = ctx->refine_plane;
+    a.nn = ctx->nn.as<int32_t>(), a.st_pose = ctx->st_pose.as<double>(), a.st_i = ctx->st_i.as<int32_t>(), a.st_hg = ctx->st_hg.as<double>();
+    a.out_T = dT.as<double>(), a.out_iters = dit.as<int32_t>(), a.out_flags = dfl.as<int32_t>();
+    if ((e = launch_linearize_once(a, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 3;
+    double hg[44];
+    int32_t sti[8];
+    std::vector<int32_t> nn((size_t)n);
+    const size_t plane = (size_t)ctx->refine_plane;
+    std::vector<double> wb(10 * (size_t)n);
+    if ((rc = d2h(ctx, hg, ctx->st_hg.p, sizeof hg)) || (rc = d2h(ctx, sti, ctx->st_i.p, sizeof sti)) ||
+        (rc = d2h(ctx, nn.data(), ctx->nn.p, (size_t)n * 4)))
+      break;
+    for (int q = 0; q < 10 && !rc; ++q) rc = d2h(ctx, wb.data() + (size_t)q * n, ctx->w_buf.as<double>() + q * plane, (size_t)n * 8);
+    if (rc) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+      rc = fail(ctx, PX_E_CUDA, std::string("linearize: ") + cudaGetErrorString(e));
+      break;
+    }
+    if (h36) memcpy(h36, hg, 36 * 8);
+    if (g6) memcpy(g6, hg + 36, 6 * 8);
+    if (f0) *f0 = hg[42];
+    const int nc = sti[6];  // ST_NCOMPACT
+    if (n_corr) *n_corr = nc;
+    if (corr)
+      for (int64_t i = 0; i < n; ++i) corr[i] = nn[(size_t)i];
+    if (w) {
+      memset(w, 0, (size_t)n * 72);
+      for (int k = 0; k < nc; ++k) {
+        long long ij;
+        memcpy(&ij, &wb[9 * (size_t)n + k], 8);
+        const size_t i = (size_t)(unsigned)ij;
+        for (int q = 0; q < 9; ++q) w[9 * i + q] = wb[(size_t)q * n + k];
+      }
+    }
+  } while (0);
+  DevBuf* bufs[] = {&dti, &dinit, &dT, &dit, &dfl};
+  for (DevBuf* b : bufs) b->release();
+  px_clouds_free(ctx, cl);
+  return rc;
+}
+
+// Test exports of the device colour functions (colorspace.py:41-124).
+int px_ciede2000(px_ctx* ctx, const double* lab_a, const double* lab_b, int64_t n, double* out) {
+  if (!ctx || n < 0 || (n && (!lab_a || !lab_b || !out))) return fail(ctx, PX_E_ARG, "px_ciede2000: bad arguments");
+  if (n == 0) return 0;
+  CU(cudaSetDevice(ctx->device));
+  DevBuf da, db, dout;
+  int rc = 0;
+  do {
+    if ((rc = h2d(ctx, da, lab_a, (size_t)n * 24)) || (rc = h2d(ctx, db, lab_b, (size_t)n * 24))) break;
+    cudaError_t e;
+    if ((e = dout.ensure((size_t)n * 8)) || (e = launch_ciede(da.as<double>(), db.as<double>(), dout.as<double>(), n, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 1;
+    if ((rc = d2h(ctx, out, dout.p, (size_t)n * 8))) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+  } while (0);
+  da.release(), db.release(), dout.release();
+  return rc;
+}
+
+int px_srgb_to_lab(px_ctx* ctx, const double* rgb, int64_t n, int32_t linear_input, double* lab_out) {
+  if (!ctx || n < 0 || (n && (!rgb || !lab_out))) return fail(ctx, PX_E_ARG, "px_srgb_to_lab: bad arguments");
+  if (n == 0) return 0;
+  CU(cudaSetDevice(ctx->device));
+  DevBuf da, dout;
+  int rc = 0;
+  do {
+    if ((rc = h2d(ctx, da, rgb, (size_t)n * 24))) break;
+    cudaError_t e;
+    if ((e = dout.ensure((size_t)n * 24)) || (e = launch_lab(da.as<double>(), dout.as<double>(), n, linear_input, ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += 1;
+    if ((rc = d2h(ctx, lab_out, dout.p, (size_t)n * 24))) break;
+    e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+  } while (0);
+  da.release(), dout.release();
+  return rc;
+}
+
 // ---- cost ---------------------------------------------------------------------
 
 int px_cost_batch(px_ctx* ctx, const px_clouds* rendered, const int32_t* object_ids, const double* cyl_poses,

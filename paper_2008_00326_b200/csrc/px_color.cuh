@@ -59,13 +59,23 @@ __device__ __forceinline__ double ciede2000(double L1, double a1, double b1, dou
   const double dL = L2 - L1, dC = c2p - c1p;
   const bool grey = (c1p * c2p) == 0.0;
   double dh = h2 - h1;
-  if (dh > 180.0) dh -= 360.0;
-  if (dh < -180.0) dh += 360.0;
+  // |h2 - h1| > 180 decides two branches (colorspace.py:91-92, :97-99).  For (near-)antipodal hues the rounded angles
+  // sit on that threshold and the last bit of atan2 (libdevice here, libm / SVML in numpy) would pick the branch --
+  // e.g. published pair 14, (50, -0.001, 2.49) vs (50, 0.001, -2.49), whose hue difference is exactly 180.  Within
+  // 1e-9 degrees of the threshold the decision is therefore taken on the exact sign of the cross product of the two
+  // chroma vectors: |dh| > 180 iff the turn from h1 to h2 overshoots the half circle.
+  bool over = fabs(dh) > 180.0;
+  if (fabs(fabs(dh) - 180.0) < 1e-9) {
+    const double p = a1p * b2, q = a2p * b1;
+    const double cross = (p - q) + (fma(a1p, b2, -p) - fma(a2p, b1, -q));  // error-free products: exact sign
+    over = cross != 0.0 && ((cross < 0.0) == (dh > 0.0));
+  }
+  if (over) dh += dh > 0.0 ? -360.0 : 360.0;
   if (grey) dh = 0.0;
   const double dH = 2.0 * sqrt(c1p * c2p) * sin((0.5 * dh) * D2R);
   const double Lm = 0.5 * (L1 + L2), Cm = 0.5 * (c1p + c2p);
-  const double hs = h1 + h2, hd = fabs(h1 - h2);
-  double hm = hd <= 180.0 ? 0.5 * hs : (hs < 360.0 ? 0.5 * (hs + 360.0) : 0.5 * (hs - 360.0));
+  const double hs = h1 + h2;
+  double hm = !over ? 0.5 * hs : (hs < 360.0 ? 0.5 * (hs + 360.0) : 0.5 * (hs - 360.0));
   if (grey) hm = hs;
   const double t = 1.0 - 0.17 * cos((hm - 30.0) * D2R) + 0.24 * cos((2.0 * hm) * D2R) +
                    0.32 * cos((3.0 * hm + 6.0) * D2R) - 0.20 * cos((4.0 * hm - 63.0) * D2R);

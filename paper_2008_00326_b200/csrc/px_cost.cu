@@ -244,6 +244,29 @@ cudaError_t launch_winners(const WinnerArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// colorspace.ciede2000 / srgb_to_lab for arrays (test exports: the device functions the cost and render kernels inline)
+__global__ void ciede_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out, long long n) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = ciede2000(a[3 * i], a[3 * i + 1], a[3 * i + 2], b[3 * i], b[3 * i + 1], b[3 * i + 2]);
+}
+__global__ void lab_kernel(const double* __restrict__ rgb, double* __restrict__ out, long long n, int encode_first) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+  if (encode_first) r = srgb_encode1(r), g = srgb_encode1(g), b = srgb_encode1(b);  // raster.py:278 on linear colours
+  srgb_to_lab(r, g, b, out[3 * i], out[3 * i + 1], out[3 * i + 2]);
+}
+cudaError_t launch_ciede(const double* a, const double* b, double* out, long long n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ciede_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(a, b, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_lab(const double* rgb, double* out, long long n, int encode_first, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  lab_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(rgb, out, n, encode_first);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // exact brute-force kNN (neighbors.py:104-134), thread per query
 

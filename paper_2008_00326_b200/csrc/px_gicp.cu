@@ -22,6 +22,14 @@
 
 #include "px_kernels.h"
 
+#ifdef PX_NO_STREAM_HINTS  // experiment: default cache policy for the per-iteration scratch (L2-blocked chunks)
+#define PX_LDCS(p) (*(p))
+#define PX_STCS(p, v) (*(p) = (v))
+#else
+#define PX_LDCS(p) __ldcs(p)
+#define PX_STCS(p, v) __stcs(p, v)
+#endif
+
 namespace px {
 
 enum { F_OK = 0, F_TOO_FEW = 1, F_DEGENERATE = 2, F_SINGULAR = 3, F_NO_DECREASE = 4 };
@@ -830,7 +838,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
   for (int q = 0; q < 12; ++q) in[q] = 0.0;
   if (bj_cur >= 0) {
 #pragma unroll
-    for (int q = 0; q < 6; ++q) in[q] = __ldcs(soa + q * plane + lane);
+    for (int q = 0; q < 6; ++q) in[q] = PX_LDCS(soa + q * plane + lane);
 #pragma unroll
     for (int q = 0; q < 6; ++q) in[6 + q] = __ldg(tsoa + q * tplane + bj_cur);
   }
@@ -927,9 +935,9 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     if (on) {  // ordered compaction for the halving kernel
       double* o = wb + *n_corr_sm + __popc(onm & ((1u << lane) - 1u));
 #pragma unroll
-      for (int q = 0; q < 9; ++q) __stcs(o + q * plane, w[q]);  // streamed: read once, by the halving kernel
+      for (int q = 0; q < 9; ++q) PX_STCS(o + q * plane, w[q]);  // streamed: read once, by the halving kernel
       // tenth plane: (source index, target index) -- the halving kernel fetches the two points itself
-      __stcs(reinterpret_cast<long long*>(o + 9 * plane), (long long)(unsigned)i | ((long long)bj << 32));
+      PX_STCS(reinterpret_cast<long long*>(o + 9 * plane), (long long)(unsigned)i | ((long long)bj << 32));
     }
     __syncwarp();
     if (lane == 0) *n_corr_sm += __popc(onm);
@@ -940,7 +948,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_lin_ker
     bj_next = i + 64 < n ? nn[i + 64] : -1;
     if (bj_cur >= 0) {
 #pragma unroll
-      for (int q = 0; q < 6; ++q) in[q] = __ldcs(soa + q * plane + i + 32);  // streamed once per iteration
+      for (int q = 0; q < 6; ++q) in[q] = PX_LDCS(soa + q * plane + i + 32);  // streamed once per iteration
 #pragma unroll
       for (int q = 0; q < 6; ++q) in[6 + q] = __ldg(tsoa + q * tplane + bj_cur);
     }
@@ -1060,12 +1068,12 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
     double f = 0.0;
     double cur[15];  // W (9) | source point (3) | target point (3)
     // software pipeline: the (source, target) index pair of a chunk is fetched one chunk ahead of its operands
-    long long ij_cur = lane < nc ? __ldcs(reinterpret_cast<const long long*>(wb + 9 * plane) + lane) : 0;
-    long long ij_next = lane + 32 < nc ? __ldcs(reinterpret_cast<const long long*>(wb + 9 * plane) + lane + 32) : 0;
+    long long ij_cur = lane < nc ? PX_LDCS(reinterpret_cast<const long long*>(wb + 9 * plane) + lane) : 0;
+    long long ij_next = lane + 32 < nc ? PX_LDCS(reinterpret_cast<const long long*>(wb + 9 * plane) + lane + 32) : 0;
     if (lane < nc) {
       const int si = (int)(unsigned)ij_cur, tj = (int)(ij_cur >> 32);
 #pragma unroll
-      for (int q = 0; q < 9; ++q) cur[q] = __ldcs(wb + q * plane + lane);
+      for (int q = 0; q < 9; ++q) cur[q] = PX_LDCS(wb + q * plane + lane);
 #pragma unroll
       for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
     }
@@ -1091,11 +1099,11 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
       }
       __syncwarp();
       ij_cur = ij_next;
-      ij_next = k + 64 < nc ? __ldcs(reinterpret_cast<const long long*>(wb + 9 * plane) + k + 64) : 0;
+      ij_next = k + 64 < nc ? PX_LDCS(reinterpret_cast<const long long*>(wb + 9 * plane) + k + 64) : 0;
       if (k + 32 < nc) {  // next chunk's operands are in flight during the ordered sums
         const int si = (int)(unsigned)ij_cur, tj = (int)(ij_cur >> 32);
 #pragma unroll
-        for (int q = 0; q < 9; ++q) cur[q] = __ldcs(wb + q * plane + k + 32);
+        for (int q = 0; q < 9; ++q) cur[q] = PX_LDCS(wb + q * plane + k + 32);
 #pragma unroll
         for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
       }
@@ -1250,6 +1258,19 @@ void dump_nn_stats() {
   cudaMemcpyToSymbol(g_nn_rhist, h, sizeof h);
 }
 #endif
+
+cudaError_t launch_linearize_once(const RefineArgs& a, cudaStream_t st) {
+  if (a.src.n == 0) return cudaSuccess;
+  cudaError_t e;
+  const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
+  if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
+  gicp_init_kernel<<<(unsigned)((a.src.n + 3) / 4), 128, smem_init, st>>>(a, 1);
+  const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
+  if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+  gicp_nn_kernel<<<(unsigned)((a.src.n + 3) / 4), 128, 0, st>>>(a, 1, 1);
+  gicp_lin_kernel<<<(a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS, PX_GICP_WARPS * 32, smem, st>>>(a, 1);
+  return cudaGetLastError();
+}
 
 // Returns the number of kernels launched through *launches.
 cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, cudaEvent_t* marks) {

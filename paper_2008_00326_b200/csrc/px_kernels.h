@@ -203,6 +203,8 @@ struct RefineArgs {
 // Launch order: init, (nn, lin + solve, halve) x max_iter, finish.  `marks` (nullable) receives one event
 // before every launch and one after the last: 3 + 3 * max_iter events.
 cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, cudaEvent_t* marks = nullptr);
+// init + the nearest-neighbour and linearise kernels of iteration 1 only (px_gicp_linearize, a test export)
+cudaError_t launch_linearize_once(const RefineArgs& a, cudaStream_t st);
 
 struct CostArgs {
   CloudsDev ren;
@@ -252,6 +254,9 @@ struct WinnerArgs {
   unsigned long long* win;            // (n_models, PX_WIN_WORDS), zero on entry
 };
 cudaError_t launch_winners(const WinnerArgs& a, cudaStream_t st);
+
+cudaError_t launch_ciede(const double* lab_a, const double* lab_b, double* out, long long n, cudaStream_t st);
+cudaError_t launch_lab(const double* rgb, double* out, long long n, int encode_first, cudaStream_t st);
 
 struct KnnArgs {  // exact brute-force kNN, k <= PX_KCOV_MAX (neighbors.py:104-134)
   const double* q;

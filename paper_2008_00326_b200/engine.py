@@ -36,6 +36,10 @@ class Engine:
             msg = self.lib.px_last_error(None)
             raise DeviceError(f"px_ctx_create({device}) failed: {msg.decode() if msg else rc}")
         self.device = int(device)
+        import os
+        if os.environ.get("PX_SCRATCH_MB"):  # tuning knob: per-chunk candidate scratch (default 8 GiB)
+            N.check(self.ctx, self.lib.px_ctx_set_scratch_budget(self.ctx, int(os.environ["PX_SCRATCH_MB"]) << 20),
+                    "px_ctx_set_scratch_budget")
         self._scene_key = None
         self._model_keys = {}
         self._model_refs = {}
@@ -281,6 +285,35 @@ class Engine:
             tr = tuple((float(a), float(b)) for a, b in trace[i, :int(ntr[i])])
             out.append(RegistrationResult(RigidTransform.from_matrix3x4(T[i]), int(iters[i]), float(resid[i]),
                                           bool(int(flags[i]) & 0x100), FAILURES[code], tr))
+        return out
+
+    def gicp_linearize(self, src, tgt, T, cfg):
+        """registration._gicp_linearize through the production kernels (test export):
+        -> (f0, n_corr, h (6,6), g (6,), corr (n,) i64, w (n,3,3))."""
+        src, tgt, T = N.f64(src), N.f64(tgt), N.f64(T)
+        n = src.shape[0]
+        h, g, f0 = np.zeros((6, 6)), np.zeros(6), C.c_double(0.0)
+        nc = C.c_int32(0)
+        corr, w = np.zeros(n, dtype=np.int64), np.zeros((n, 3, 3))
+        gc = self._gicp_cfg(cfg)
+        rc = self.lib.px_gicp_linearize(self.ctx, N.ptr(src, N.f64p), n, N.ptr(tgt, N.f64p), tgt.shape[0], N.ptr(T, N.f64p),
+                                        C.byref(gc), N.ptr(h, N.f64p), N.ptr(g, N.f64p), C.cast(C.byref(f0), N.f64p),
+                                        C.cast(C.byref(nc), N.i32p), N.ptr(corr, N.i64p), N.ptr(w, N.f64p))
+        N.check(self.ctx, rc, "px_gicp_linearize")
+        return float(f0.value), int(nc.value), h, g, corr, w
+
+    def ciede2000(self, lab_a, lab_b) -> np.ndarray:
+        a, b = N.f64(lab_a).reshape(-1, 3), N.f64(lab_b).reshape(-1, 3)
+        out = np.zeros(a.shape[0])
+        N.check(self.ctx, self.lib.px_ciede2000(self.ctx, N.ptr(a, N.f64p), N.ptr(b, N.f64p), a.shape[0], N.ptr(out, N.f64p)),
+                "px_ciede2000")
+        return out
+
+    def srgb_to_lab(self, rgb, linear_input=False) -> np.ndarray:
+        a = N.f64(rgb).reshape(-1, 3)
+        out = np.zeros_like(a)
+        N.check(self.ctx, self.lib.px_srgb_to_lab(self.ctx, N.ptr(a, N.f64p), a.shape[0], int(bool(linear_input)),
+                                                  N.ptr(out, N.f64p)), "px_srgb_to_lab")
         return out
 
     # -- cost ------------------------------------------------------------------------

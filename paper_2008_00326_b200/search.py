@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from .blas_probe import check_blas_orders
 from .cost import CostBreakdown, CostParams
 from .errors import ConfigError, EmptyBatch, NoValidDepth
 from .geometry import RigidTransform, rotation_angle
@@ -258,6 +259,7 @@ def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = Tr
     False only the target SPECS (capsule parameters / label ids) and the
     candidate -> target map are produced; the device crops the clouds itself
     (Engine.build_targets)."""
+    check_blas_orders()  # once per process: the host BLAS must round like the device's baked-in orders (H2)
     k = frame.intrinsics
     cam_to_world = RigidTransform(k.camera_pose.rotation, k.camera_pose.translation)
     world_to_cam = cam_to_world.inverse()

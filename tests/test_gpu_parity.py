@@ -127,6 +127,10 @@ def test_m2m_gicp_failure_slots(engine):
     assert out[2].failure == "degenerate_correspondences" and out[2].iterations == 1
 
 
+# candidates whose GICP iteration is chaotic under last-bit differences of the linear solve / libm
+# (reference 16 iterations, restated arithmetic 30): 1 of 1,500 in C3, none elsewhere
+KNOWN_CHAOTIC = {"c3_clutter_3dof": {1131}}
+
 SEARCH = ["c1_box_3dof", "c2_twocyl_color1", "c2_twocyl_color0", "c3_clutter_3dof", "c3n_clutter_noisy", "c4_mixed_6dof"]
 
 
@@ -216,12 +220,18 @@ def test_search_matches_oracle_and_reference(engine, runs, name):
     same = (dev.j_o == cpu.j_o) & (dev.j_r == cpu.j_r)
     same_ref = (dev.j_o == d["j_o"]) & (dev.j_r == d["j_r"])
     it_eq = dev.iterations == cpu.iterations
-    print(f"{name}: n={plan.n} pose-agree(oracle)={close.mean():.4f} iters-equal={it_eq.mean():.4f} "
-          f"costs-equal(oracle)={same.mean():.4f} costs-equal(reference)={same_ref.mean():.4f} "
-          f"max dt={dt.max():.3e}")
-    assert close.mean() >= 0.95
-    assert same[close & (dt == 0) & (dr == 0)].all()
-    assert same.mean() >= 0.95 and same_ref.mean() >= 0.75
+    rt, rr = G.pose_delta(dev.refined_cam, d["refined"])
+    close_ref = (rt <= 1e-4) & (rr <= 1e-4)
+    print(f"{name}: n={plan.n} pose-agree(oracle)={close.mean():.4f} pose-agree(reference)={close_ref.mean():.4f} "
+          f"iters-equal={it_eq.mean():.4f} costs-equal(oracle)={same.mean():.4f} costs-equal(reference)={same_ref.mean():.4f} "
+          f"max dt={dt.max():.3e}; divergent vs oracle {np.nonzero(~close)[0].tolist()}, vs reference {np.nonzero(~close_ref)[0].tolist()}")
+    # Pinned to what is measured: every candidate of every fixture agrees with the oracle AND the
+    # reference in pose (1e-4 m / 1e-4 rad) and in both integer costs, except the ONE chaotic candidate of C3 named in
+    # KNOWN_CHAOTIC, on which the reference (LAPACK dgesv / libm) and the restated arithmetic part ways.
+    known = KNOWN_CHAOTIC.get(name, set())
+    assert set(np.nonzero(~close)[0].tolist()) <= known and set(np.nonzero(~close_ref)[0].tolist()) <= known
+    assert set(np.nonzero(~same)[0].tolist()) <= known and set(np.nonzero(~same_ref)[0].tolist()) <= known
+    assert set(np.nonzero(~it_eq)[0].tolist()) <= known
     a = json.loads(result_to_json(assemble_result(plan, dev, 0.0)))
     b = json.loads(result_to_json(assemble_result(plan, cpu, 0.0)))
     ref = json.loads(str(d["result_json"]))
@@ -575,8 +585,8 @@ def test_full_size_sample_against_oracle(engine):
     same = (dev.j_o == cpu.j_o) & (dev.j_r == cpu.j_r)
     print(f"full-size sample: n={pick.size} pose-agree={close.mean():.4f} iters-equal={(dev.iterations == cpu.iterations).mean():.4f} "
           f"costs-equal={same.mean():.4f}")
-    assert close.mean() >= 0.99 and (dev.iterations == cpu.iterations).mean() >= 0.99
-    assert same[close].all()
+    # pinned to the measured value: all 3,008 sampled candidates agree (poses, iteration counts, integer costs)
+    assert close.all() and (dev.iterations == cpu.iterations).all() and same.all()
 
 
 def test_full_size_6dof_sample_against_oracle(engine):
@@ -595,4 +605,4 @@ def test_full_size_6dof_sample_against_oracle(engine):
     same = (dev.j_o == cpu.j_o) & (dev.j_r == cpu.j_r)
     print(f"full-size 6-DoF sample: n={pick.size} pose-agree={close.mean():.4f} "
           f"iters-equal={(dev.iterations == cpu.iterations).mean():.4f} costs-equal={same.mean():.4f}")
-    assert close.mean() >= 0.99 and same[close].all()
+    assert close.all() and (dev.iterations == cpu.iterations).all() and same.all()  # measured: 3,009 of 3,009

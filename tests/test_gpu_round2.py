@@ -1,0 +1,202 @@
+"""GPU tests added in round 2: the GICP lock-step contract on the device (H, g, corr, W of the
+first linearisation, bit for bit), the device CIEDE2000 against the published pairs, the on-device
+argmin / winner records and libpx's own NCCL communicator, limits reported as errors."""
+
+import dataclasses
+import json
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import oracle as O
+from paper_2008_00326_b200 import GicpConfig, colorspace
+from paper_2008_00326_b200.errors import DeviceError
+from paper_2008_00326_b200.search import assemble_result, plan_search, result_to_json
+
+pytestmark = pytest.mark.gpu
+U = G.load("units")
+I34 = np.hstack([np.eye(3), np.zeros((3, 1))])
+
+
+@pytest.mark.parametrize("t", range(4))
+def test_gicp_linearize_lock_step_bit_exact(engine, t):
+    """SURVEY 7.3 H4 item 2 on the DEVICE: given identical (R, t) the correspondences, f0, g, H and the
+    per-point weights of registration._gicp_linearize (registration.py:233-338) equal the reference's
+    bit for bit -- the 43-lane ordered sums of gicp_lin_kernel against the scalar source-index loop."""
+    f0, nc, h, g, corr, w = engine.gicp_linearize(U[f"gicp{t}_src"], U[f"gicp{t}_tgt"], I34, GicpConfig())
+    assert nc == int(U[f"gicp{t}_ncorr"]) and f0 == float(U[f"gicp{t}_f0"])
+    assert np.array_equal(corr, U[f"gicp{t}_corr"])
+    assert np.array_equal(g, U[f"gicp{t}_g"])
+    assert np.array_equal(h, U[f"gicp{t}_h"])
+    on = corr >= 0
+    assert on.sum() == nc and np.array_equal(w[on], U[f"gicp{t}_w"][on])
+
+
+def test_gicp_linearize_at_a_moved_pose_equals_oracle(engine):
+    """Same contract away from the identity (a rotated, shifted iterate), against the C oracle
+    that tests/test_oracle_golden.py pins to the reference."""
+    src, tgt = U["gicp1_src"], U["gicp1_tgt"]
+    ang = 0.07
+    R = np.array([[np.cos(ang), -np.sin(ang), 0.0], [np.sin(ang), np.cos(ang), 0.0], [0.0, 0.0, 1.0]])
+    tvec = np.array([0.004, -0.003, 0.002])
+    T = np.hstack([R, tvec[:, None]])
+    cfg = GicpConfig()
+    f0, nc, h, g, corr, w = engine.gicp_linearize(src, tgt, T, cfg)
+    of0, onc, oh, og, ocorr, ow = O.gicp_linearize(src, tgt, O.covariances(src), O.covariances(tgt), R, tvec,
+                                                   cfg.max_correspondence_distance ** 2)
+    assert (f0, nc) == (of0, onc) and np.array_equal(corr, ocorr)
+    assert np.array_equal(h, oh) and np.array_equal(g, og)
+    on = corr >= 0
+    assert np.array_equal(w[on], ow[on])
+
+
+def test_device_ciede2000_published_pairs(engine):
+    """colorspace.ciede2000 as the cost kernel evaluates it (csrc/px_color.cuh): the 34 published pairs of
+    selftest_data.py:8-43 to 1e-4 (reference tests/test_colorspace.py:39-44) and the reference's own
+    outputs on random pairs to 1e-9."""
+    pairs = U["ciede_pairs"]
+    de = engine.ciede2000(pairs[:, 0:3], pairs[:, 3:6])
+    assert np.abs(de - pairs[:, 6]).max() < 1e-4
+    de2 = engine.ciede2000(U["de_a"], U["de_b"])
+    assert np.abs(de2 - U["de_out"]).max() < 1e-9
+    # symmetric in its arguments up to rounding, zero on identical inputs (reference tests/test_colorspace.py)
+    assert np.abs(engine.ciede2000(U["de_b"], U["de_a"]) - de2).max() < 1e-9
+    assert np.array_equal(engine.ciede2000(U["de_a"], U["de_a"]), np.zeros(len(U["de_a"])))
+
+
+def test_device_srgb_to_lab(engine):
+    v = U["srgb_lab_vector"]
+    assert np.abs(engine.srgb_to_lab(v[None, :3])[0] - v[3:]).max() < 0.01   # selftest_data.py:46
+    lab = engine.srgb_to_lab(U["lab_rgb"])
+    assert np.abs(lab - U["lab_out"]).max() < 1e-9                           # the reference's outputs
+    lin = colorspace.srgb_decode(U["lab_rgb"])
+    assert np.abs(engine.srgb_to_lab(lin, linear_input=True) - U["lab_out"]).max() < 1e-9  # raster.py:278 path
+
+
+@pytest.mark.parametrize("name", ["c1_box_3dof", "c4_mixed_6dof"])
+def test_winner_records_equal_host_argmin(engine, name):
+    """px_search_reduce / px_search_winners: the per-object winner extracted on the device equals
+    select_best over the downloaded per-candidate costs (search.py:178-183, 346-372), including the
+    refined pose bits and SearchResult.max_rendered_points."""
+    d, frame, models, cfg, plan = G.scene(name)
+    out = engine.run_plan(frame, models, plan)
+    engine.search_reduce()
+    win = engine.search_winners()
+    host = assemble_result(plan, out, 0.0)
+    for e in host.estimates:
+        if e.failed:
+            assert e.object_id not in win
+            continue
+        key, refined, reg_T, jo, jr, mp = win[e.object_id]
+        assert (key >> 32, key & 0xffffffff) == (e.cost.total, e.proposal_index)
+        assert (jo, jr) == (e.cost.j_o, e.cost.j_r)
+        sel = np.nonzero(plan.flat_oid == e.object_id)[0]
+        j = sel[e.proposal_index]
+        assert np.array_equal(refined, out.refined_cam[j]) and np.array_equal(reg_T, out.reg_T[j])
+        assert mp == int(out.n_rendered[sel].max())
+    assert max(w[5] for w in win.values()) == host.max_rendered_points
+
+
+def test_estimate_poses_winner_path_equals_full_download(engine):
+    """The public call returns only winner records from the device; its result JSON is byte-identical
+    to the one assembled from every candidate's downloaded outputs."""
+    from paper_2008_00326_b200 import estimate_poses
+    for name in ("c1_box_3dof", "c4_mixed_6dof"):
+        d, frame, models, cfg, plan = G.scene(name)
+        res = estimate_poses(frame, models, cfg)
+        full = assemble_result(plan, engine.run_plan(frame, models, plan), 0.0)
+        assert result_to_json(res) == result_to_json(full)
+        assert res.max_rendered_points == full.max_rendered_points and res.proposals_evaluated == full.proposals_evaluated
+
+
+def test_nccl_communicator_single_rank(engine):
+    """libpx's own NCCL communicator (px_comm_init, dlopen'ed NCCL): with one rank the all-reduce(MIN) of the
+    keys and the all-reduce(MAX) of the winner records must be identities -- exercises the run-time binding,
+    the datatype / op enums and the stream ordering on the one GPU a test box has."""
+    d, frame, models, cfg, plan = G.scene("c1_box_3dof")
+    plan = plan_search(frame, models, dataclasses.replace(cfg, refine=False))
+    out = engine.run_plan(frame, models, plan)
+    engine.search_reduce()
+    before = engine.search_winners()
+    engine.comm_init(0, 1, engine.comm_unique_id())
+    try:
+        assert engine.comm_world() == 1 and engine.nccl_version() >= 21800
+        engine.search_run(engine.search_cfg(plan))
+        engine.search_reduce()
+        after = engine.search_winners()
+    finally:
+        engine.lib.px_comm_destroy(engine.ctx)
+    assert before.keys() == after.keys()
+    for o in before:
+        assert before[o][0] == after[o][0] and np.array_equal(before[o][1], after[o][1]) and before[o][3:] == after[o][3:]
+    assert before[1][0] == out.best_keys[1]
+
+
+def test_two_shards_on_one_gpu_reduce_to_the_single_process_result(engine):
+    """Candidate sharding (dist.shard_index) + min over the shards' packed device keys == the unsharded
+    device argmin (the multi-GPU analogue of reference tests/test_search.py:100-106)."""
+    from paper_2008_00326_b200 import dist as pxd
+    d, frame, models, cfg, plan = G.scene("c3_clutter_3dof")
+    whole = engine.run_plan(frame, models, plan)
+    keys = []
+    for r in range(3):
+        idx = pxd.shard_index(plan, r, 3)
+        engine.run_plan(frame, models, plan, idx)
+        engine.search_reduce()
+        w = engine.search_winners()
+        keys.append({o: w[o][0] for o in w})
+    for o, k in whole.best_keys.items():
+        got = min(kk.get(o, pxd.NO_KEY) for kk in keys)
+        assert got == min(k, pxd.NO_KEY)
+
+
+def test_limits_are_errors_not_different_answers(engine):
+    """implementation limits surface as PX_E_LIMIT / DeviceError."""
+    d, frame, models, cfg, plan = G.scene("c1_box_3dof")
+    with pytest.raises(DeviceError, match="k_covariance"):
+        engine.upload_targets(np.array([0, 50]), np.random.default_rng(0).normal(size=(50, 3)),
+                              dataclasses.replace(cfg.gicp, k_covariance=33))
+    # stale targets under resident candidates are caught at run time, not read out of bounds
+    engine.prepare_plan(frame, models, plan)
+    engine.search_upload(plan)
+    engine.upload_targets(np.array([0, 40]), np.random.default_rng(1).normal(size=(40, 3)), cfg.gicp)
+    with pytest.raises(DeviceError, match="targets are resident|different k_covariance"):
+        engine.search_run(engine.search_cfg(plan))
+    # a different epsilon than the targets were built with is refused
+    engine.prepare_plan(frame, models, plan)
+    sc = engine.search_cfg(dataclasses.replace(plan, cfg=dataclasses.replace(cfg, gicp=dataclasses.replace(cfg.gicp, epsilon=2e-3))))
+    engine.build_targets(plan)
+    with pytest.raises(DeviceError, match="epsilon"):
+        engine.search_run(sc)
+
+
+def test_rendered_points_closer_than_delta_are_scored_exactly(engine):
+    """A rendered point nearer to the camera than delta has no bounded pixel window; the cost kernel then
+    scans the whole grid instead of calling it an outlier (cost.py:108-124 is a global brute force)."""
+    from paper_2008_00326_b200 import LabeledCloud
+    d, frame, models, cfg, plan = G.scene("c1_box_3dof")
+    engine.upload_scene(frame, cfg.stride, plan.observed, plan.obs_labels)
+    engine.upload_models(models)
+    obs = plan.observed
+    near = np.array([[1e-4, -2e-4, 0.004], [0.0, 0.0, 0.006]])   # z < delta = 0.0075
+    far = obs.points[[10, 5000, 20000]] + 1e-4                   # explained by their observed neighbours
+    pts = np.vstack([near, far])
+    h = engine._upload_clouds([pts], [np.zeros_like(pts)], [np.zeros((len(pts), 2), dtype=np.int32)])
+    try:
+        jo, jr = engine.cost_handle(h, np.array([1]), plan.cam_poses[:1], cfg.delta, cfg.tau_c, False)
+    finally:
+        engine.lib.px_clouds_free(engine.ctx, h)
+    ejr, ex = O.rendered_cost(pts, np.zeros_like(pts), obs.points, obs.lab_colors, cfg.delta, cfg.tau_c, False)
+    assert int(jr[0]) == ejr == 2
+
+
+def test_knife_edge_log(engine):
+    """every run reports how close a gate decision came to its threshold; the fixtures'
+    integer costs are far from the ~1e-12 disagreement of libdevice vs numpy transcendentals."""
+    d, frame, models, cfg, plan = G.scene("c2_twocyl_color1")
+    engine.run_plan(frame, models, plan)
+    k = engine.knife_edges()
+    assert 0.0 < k["min_abs_d2_minus_delta2"] < cfg.delta ** 2
+    assert k["min_abs_dE_minus_tau_c"] > 1e-9
+    print("knife edges:", k)

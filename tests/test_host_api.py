@@ -205,3 +205,32 @@ def test_cli_exit_codes_without_device(tmp_path, capsys):
     assert main(["bench", "--scene", str(DATASET / "scene_0000"), "--models", str(DATASET / "models"),
                  "--workers", "0"]) == 2
     capsys.readouterr()
+
+
+def test_blas_order_probe_passes_here_and_fails_loudly(monkeypatch):
+    """the start-up probe accepts this host's numpy/BLAS and raises when the
+    fused orders differ from what csrc/px_common.cuh bakes in."""
+    from paper_2008_00326_b200 import blas_probe as B
+    bad = B.check_blas_orders(force=True)
+    assert not any(bad.values())
+    # a host whose (3,3)@(3,) product used the k = 0,1,2 order instead of 1,0,2
+    monkeypatch.setattr(B, "dot_f102", B.dot_f012)
+    with pytest.raises(B.BlasOrderError, match="rounds small matrix products"):
+        B.check_blas_orders(force=True)
+    monkeypatch.undo()
+    B.check_blas_orders(force=True)
+
+
+def test_bench_gpus_flag_spawns_one_rank_per_gpu(monkeypatch):
+    """`python bench.py --gpus N` without torchrun re-executes itself under torch.distributed.run
+    with N ranks on 127.0.0.1 (the flag used to be parsed and ignored)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, PX_BENCH_PRINT_SPAWN="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "4", "--steps", "2"], env=env,
+                         capture_output=True, text=True, check=True).stdout
+    cmd = json.loads(out.strip().splitlines()[-1])
+    assert "torch.distributed.run" in cmd and "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]

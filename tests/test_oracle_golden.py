@@ -191,8 +191,12 @@ def test_oracle_search_matches_reference(name, oracle_runs):
     print(f"{name}: poses within 1e-4 m/rad {close.mean():.4f}; integer costs equal {same_cost.mean():.4f}")
     if cfg.refine:
         assert np.array_equal(out.iterations == 0, d["reg_iters"] == 0)
-        assert close.mean() >= 0.75          # reference self-agreement under 4-ulp noise is ~0.81
-        assert same_cost[close].all()        # identical pose => identical integers
+        # pinned to what is measured: every candidate except the one chaotic C3 candidate (index 1131: the reference
+        # stops after 16 iterations, the restated LU / libm arithmetic runs 30); the reference's own self-agreement
+        # under 4-ulp input noise is only ~0.81, so this is as tight as the domain allows
+        known = {"c3_clutter_3dof": {1131}}.get(name, set())
+        assert set(np.nonzero(~close)[0].tolist()) <= known
+        assert set(np.nonzero(~same_cost)[0].tolist()) <= known
     else:
         assert close.all() and same_cost.all()
     ref = json.loads(str(d["result_json"]))
