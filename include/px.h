@@ -92,6 +92,16 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
                     const int32_t* labels, const double intr[4] /* fx fy cx cy */, int32_t stride,
                     const double* obs_points, const double* obs_lab, const int32_t* obs_src_px,
                     const int32_t* obs_labels, int64_t n_obs);
+/* Same, with the observed cloud built ON THE DEVICE from the frame (replaces raster.frame_to_cloud /
+ * _grid_cloud / cloud_labels, raster.py:191-217): stride-grid sampling of `valid`, row-major order,
+ * unprojection at the pixel centre, sRGB -> Lab, label per point.  color_grid is the (GH,GW,3) float64
+ * sRGB image of the stride-grid pixels (frame.color[::stride, ::stride]).  Points, source pixels and labels
+ * are bit-identical to the host path; Lab agrees to ~1e-12.  n_obs_out (nullable) receives the cloud size. */
+int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
+                          const int32_t* labels, const double* color_grid, const double intr[4], int32_t stride,
+                          int64_t* n_obs_out);
+/* The resident observed cloud (any pointer may be NULL): points (n,3), Lab (n,3), source pixels (n,2), labels (n). */
+int px_scene_download_cloud(px_ctx* ctx, double* points, double* lab, int32_t* src_px, int32_t* labels);
 /* ObjectModel (model.py:75-85): mesh with colours already decoded to linear light
  * (colorspace.srgb_decode, done once per model on the host), inscribed cylinder
  * as (radius**2, z_min, z_max).  Re-uploading an id replaces it. */
@@ -188,6 +198,29 @@ int px_knn(px_ctx* ctx, const double* queries, int64_t nq, const double* targets
  * candidate's position among its object's candidates (select_best's index). */
 int px_search_upload(px_ctx* ctx, int64_t n, const int32_t* object_ids, const double* poses3x4,
                      const int32_t* target_idx, const int32_t* rank_in_object);
+/* Candidates generated ON THE DEVICE from the proposal lattice (replaces the per-candidate host work of
+ * search.py:240-257, proposals.py:163-210): every object's hypotheses are an outer x inner product --
+ *   3-DoF: outer = grid cells (translations (n_outer,3) = x, y, fixed_z), inner = yaw spins (rotations (n_inner,9));
+ *          camera pose = world_to_cam o [spin | cell] in the host BLAS rounding order (w2c_vec_order as in px_search_cfg);
+ *   6-DoF: outer = rotations (n_outer,9), inner = translations (n_inner,3), already in the camera frame
+ * -- with the inner index fastest and rank_in_object = outer * n_inner + inner, exactly the flat order of
+ * PoseProposalSet.  Only outer items with (outer index % world) == rank are generated (the shard of one rank,
+ * parallel.py:28-37's worker split; world = 1: everything).  With `gicp` non-NULL the GICP targets are built as well:
+ * 3-DoF one capsule {cell x, cell y, capsule[0] = z_lo, capsule[1] = z_hi, capsule[2] = radius} per local (object, cell)
+ * (search.py:407-426), 6-DoF one label sub-cloud per object.  Objects must have been uploaded (px_model_upload). */
+typedef struct {
+  int32_t object_id;
+  int32_t n_outer, n_inner;
+  const double* rotations;
+  const double* translations;
+  double capsule[3];
+} px_lattice;
+int px_search_upload_lattice(px_ctx* ctx, int32_t mode3dof, int32_t n_objects, const px_lattice* objs,
+                             const double world_to_cam[12], int32_t w2c_vec_order, const double cam_to_world[12],
+                             const px_gicp_cfg* gicp /* nullable: no refinement */, int32_t rank, int32_t world,
+                             int64_t* n_local_out);
+/* The resident candidates (any pointer may be NULL): model slot, pose (n,12), target index, rank in object. */
+int px_search_candidates(px_ctx* ctx, int32_t* model_slot, double* poses3x4, int32_t* target_idx, int32_t* rank_in_object);
 /* Run render -> refine -> re-render -> cost -> per-object argmin on the resident
  * candidates; results stay on the device.  Asynchronous only in the sense that
  * stage timing uses CUDA events on the context stream; returns after the last

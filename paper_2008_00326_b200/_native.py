@@ -37,6 +37,11 @@ class SearchCfg(C.Structure):
                 ("fixed_z", C.c_double)]
 
 
+class Lattice(C.Structure):
+    _fields_ = [("object_id", C.c_int32), ("n_outer", C.c_int32), ("n_inner", C.c_int32),
+                ("rotations", f64p), ("translations", f64p), ("capsule", C.c_double * 3)]
+
+
 _SIGS = {
     "px_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
     "px_ctx_destroy": (None, [vp]),
@@ -47,6 +52,11 @@ _SIGS = {
     "px_ctx_launch_count": (C.c_int64, [vp]),
     "px_scene_upload": (C.c_int, [vp, C.c_int32, C.c_int32, f64p, u8p, i32p, f64p, C.c_int32,
                                   f64p, f64p, i32p, i32p, C.c_int64]),
+    "px_scene_upload_frame": (C.c_int, [vp, C.c_int32, C.c_int32, f64p, u8p, i32p, f64p, f64p, C.c_int32, i64p]),
+    "px_scene_download_cloud": (C.c_int, [vp, f64p, f64p, i32p, i32p]),
+    "px_search_upload_lattice": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(Lattice), f64p, C.c_int32, f64p,
+                                           C.POINTER(GicpCfg), C.c_int32, C.c_int32, i64p]),
+    "px_search_candidates": (C.c_int, [vp, i32p, f64p, i32p, i32p]),
     "px_model_upload": (C.c_int, [vp, C.c_int32, f64p, f64p, i32p, C.c_int64, C.c_int64, f64p]),
     "px_render_batch": (C.c_int, [vp, i32p, f64p, C.c_int64, C.c_int32, C.c_double, C.POINTER(vp)]),
     "px_clouds_count": (C.c_int64, [vp]),

@@ -73,6 +73,9 @@ struct px_ctx {
   int64_t n_obs = 0;
   DevBuf depth, valid, labels, obs_pts, obs_lab, obs_labels, obs_cell, gx, gy, gz, gidx;
   std::vector<int32_t> h_obs_labels, h_obs_src;
+  bool obs_host_stale = false;  // the observed cloud was built on the device (px_scene_upload_frame): host copies lazily
+  DevBuf obs_src, color_grid, row_cnt, row_off;
+  DevBuf lat_objs, lat_rot, lat_tr;
   // models
   std::vector<ModelHost*> models;
   std::map<int32_t, int> slot_of;
@@ -152,11 +155,17 @@ int sync_models(px_ctx* ctx) {
     md[i].cyl_r2 = m->cyl[0], md[i].cyl_zmin = m->cyl[1], md[i].cyl_zmax = m->cyl[2];
     md[i].aabb_r = std::sqrt(m->cyl[0]) * (1.0 + 1e-9);
     smem = std::max(smem, render_smem_bytes(m->V, m->T));
-    for (int32_t l : ctx->h_obs_labels) lc[i] += (l == m->object_id);
+    if (!ctx->obs_host_stale)
+      for (int32_t l : ctx->h_obs_labels) lc[i] += (l == m->object_id);
   }
   ctx->render_smem = smem;
   if (int r = h2d(ctx, ctx->models_dev, md.data(), md.size() * sizeof(ModelDev))) return r;
   if (int r = h2d(ctx, ctx->label_count, lc.data(), lc.size() * sizeof(int32_t))) return r;
+  if (ctx->obs_host_stale) {  // the labels of the observed cloud live on the device only
+    CU(launch_label_count(ctx->obs_labels.as<int32_t>(), ctx->n_obs, ctx->models_dev.as<ModelDev>(), (int)md.size(),
+                          ctx->label_count.as<int32_t>(), ctx->stream));
+    ctx->launches += 1;
+  }
   CU(cudaStreamSynchronize(ctx->stream));  // md / lc are stack-owned
   ctx->models_dirty = false;
   return 0;
@@ -309,6 +318,31 @@ int ensure_refine_scratch(px_ctx* ctx, long long total_cap, int64_t n_cand) {
   return 0;
 }
 
+int set_camera(px_ctx* ctx, int32_t H, int32_t W, const double intr[4], int32_t stride) {
+  if ((W + stride - 1) / stride > PX_TILE_PIX)
+    return fail(ctx, PX_E_LIMIT, "image rows wider than " + std::to_string(PX_TILE_PIX) + " stride-grid pixels do not fit the z-buffer tile");
+  Camera& c = ctx->cam;
+  c.fx = intr[0], c.fy = intr[1], c.cx = intr[2], c.cy = intr[3];
+  c.W = W, c.H = H, c.stride = stride;
+  c.GW = (W + stride - 1) / stride, c.GH = (H + stride - 1) / stride;
+  // bound of 1 + a^2 + b^2 over all pixel centres of the image (normalised coordinates)
+  const double am = std::max(c.cx, (double)W - c.cx) / c.fx, bm = std::max(c.cy, (double)H - c.cy) / c.fy;
+  c.ray_k = (double)stride / (std::max(c.fx, c.fy) * std::sqrt(1.0 + am * am + bm * bm)) * (1.0 - 1e-9);
+  return 0;
+}
+
+// host copies of the observed labels / source pixels (needed by px_targets_upload's organised check only)
+int fetch_obs_host(px_ctx* ctx) {
+  if (!ctx->obs_host_stale) return 0;
+  ctx->h_obs_labels.resize((size_t)ctx->n_obs);
+  ctx->h_obs_src.resize(2 * (size_t)ctx->n_obs);
+  if (int r = d2h(ctx, ctx->h_obs_labels.data(), ctx->obs_labels.p, (size_t)ctx->n_obs * 4)) return r;
+  if (int r = d2h(ctx, ctx->h_obs_src.data(), ctx->obs_src.p, (size_t)ctx->n_obs * 8)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->obs_host_stale = false;
+  return 0;
+}
+
 // ---- NCCL, bound at run time (no link-time dependency: torch ships libnccl.so.2) ----------------
 struct px_nccl_id {
   char internal[128];  // ncclUniqueId (NCCL_UNIQUE_ID_BYTES)
@@ -397,6 +431,8 @@ void px_ctx_destroy(px_ctx* ctx) {
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1, &ctx->r_nm, &ctx->r_nfp};
   for (DevBuf* b : bufs) b->release();
   ctx->r_win.release(), ctx->r_knife.release();
+  ctx->obs_src.release(), ctx->color_grid.release(), ctx->row_cnt.release(), ctx->row_off.release();
+  ctx->lat_objs.release(), ctx->lat_rot.release(), ctx->lat_tr.release();
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
   ctx->comm = nullptr;
   ctx->clouds.release();
@@ -439,18 +475,10 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   if (!ctx) return PX_E_ARG;
   if (H <= 0 || W <= 0 || stride < 1 || !depth || !valid || !labels || !intr || n_obs < 0)
     return fail(ctx, PX_E_ARG, "px_scene_upload: bad arguments");
-  if ((W + stride - 1) / stride > PX_TILE_PIX)
-    return fail(ctx, PX_E_LIMIT, "image rows wider than " + std::to_string(PX_TILE_PIX) + " stride-grid pixels do not fit the z-buffer tile");
   CU(cudaSetDevice(ctx->device));
+  if (int r = set_camera(ctx, H, W, intr, stride)) return r;
   Camera& c = ctx->cam;
-  c.fx = intr[0], c.fy = intr[1], c.cx = intr[2], c.cy = intr[3];
-  c.W = W, c.H = H, c.stride = stride;
-  c.GW = (W + stride - 1) / stride, c.GH = (H + stride - 1) / stride;
-  {
-    // bound of 1 + a^2 + b^2 over all pixel centres of the image (normalised coordinates)
-    const double am = std::max(c.cx, (double)W - c.cx) / c.fx, bm = std::max(c.cy, (double)H - c.cy) / c.fy;
-    c.ray_k = (double)stride / (std::max(c.fx, c.fy) * std::sqrt(1.0 + am * am + bm * bm)) * (1.0 - 1e-9);
-  }
+  ctx->obs_host_stale = false;
   const size_t npix = (size_t)H * W;
   if (int r = h2d(ctx, ctx->depth, depth, npix * sizeof(double))) return r;
   if (int r = h2d(ctx, ctx->valid, valid, npix)) return r;
@@ -499,6 +527,77 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   ctx->have_scene = true;
   ctx->models_dirty = true;  // label counts depend on the scene
   ctx->bitmap_slots = 0;     // grid size may have changed
+  return 0;
+}
+
+int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
+                          const int32_t* labels, const double* color_grid, const double intr[4], int32_t stride,
+                          int64_t* n_obs_out) {
+  if (!ctx) return PX_E_ARG;
+  if (H <= 0 || W <= 0 || stride < 1 || !depth || !valid || !labels || !color_grid || !intr)
+    return fail(ctx, PX_E_ARG, "px_scene_upload_frame: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  if (int r = set_camera(ctx, H, W, intr, stride)) return r;
+  const Camera& c = ctx->cam;
+  const size_t npix = (size_t)H * W, ng = (size_t)c.GW * c.GH;
+  if (int r = h2d(ctx, ctx->depth, depth, npix * sizeof(double))) return r;
+  if (int r = h2d(ctx, ctx->valid, valid, npix)) return r;
+  if (int r = h2d(ctx, ctx->labels, labels, npix * sizeof(int32_t))) return r;
+  if (int r = h2d(ctx, ctx->color_grid, color_grid, ng * 24)) return r;
+  CU(ctx->row_cnt.ensure((size_t)c.GH * 8));
+  CU(ctx->row_off.ensure((size_t)c.GH * 8));
+  SceneCloudArgs a{};
+  a.H = H, a.W = W, a.stride = stride, a.GW = c.GW, a.GH = c.GH;
+  a.fx = c.fx, a.fy = c.fy, a.cx = c.cx, a.cy = c.cy;
+  a.depth = ctx->depth.as<double>(), a.valid = ctx->valid.as<uint8_t>(), a.labels = ctx->labels.as<int32_t>();
+  a.color_grid = ctx->color_grid.as<double>();
+  a.row_count = ctx->row_cnt.as<long long>(), a.row_offset = ctx->row_off.as<long long>();
+  CU(launch_scene_count(a, ctx->stream));
+  CU(launch_scan(a.row_count, ctx->row_off.as<long long>(), ctx->total_dev.as<long long>(), c.GH, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->total_host, ctx->total_dev.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  const int64_t n_obs = *ctx->total_host;
+  const size_t n1 = (size_t)std::max<int64_t>(n_obs, 1);
+  CU(ctx->obs_pts.ensure(n1 * 24));
+  CU(ctx->obs_lab.ensure(n1 * 24));
+  CU(ctx->obs_src.ensure(n1 * 8));
+  CU(ctx->obs_labels.ensure(n1 * 4));
+  CU(ctx->obs_cell.ensure(n1 * 4));
+  CU(ctx->gx.ensure(ng * 8));
+  CU(ctx->gy.ensure(ng * 8));
+  CU(ctx->gz.ensure(ng * 8));
+  CU(ctx->gidx.ensure(ng * 4));
+  a.pts = ctx->obs_pts.as<double>(), a.lab = ctx->obs_lab.as<double>(), a.src = ctx->obs_src.as<int32_t>();
+  a.labels_out = ctx->obs_labels.as<int32_t>(), a.cell = ctx->obs_cell.as<int32_t>();
+  a.gx = ctx->gx.as<double>(), a.gy = ctx->gy.as<double>(), a.gz = ctx->gz.as<double>(), a.gidx = ctx->gidx.as<int32_t>();
+  CU(launch_scene_fill(a, ctx->stream));
+  ctx->launches += 3;
+  ctx->n_obs = n_obs;
+  ctx->organised = true, ctx->have_scene = true;
+  ctx->obs_host_stale = true;
+  ctx->h_obs_labels.clear(), ctx->h_obs_src.clear();
+  ctx->models_dirty = true;
+  ctx->bitmap_slots = 0;
+  if (n_obs_out) *n_obs_out = n_obs;
+  return 0;
+}
+
+int px_scene_download_cloud(px_ctx* ctx, double* points, double* lab, int32_t* src_px, int32_t* labels) {
+  if (!ctx || !ctx->have_scene) return fail(ctx, PX_E_ARG, "px_scene_download_cloud: no scene");
+  const size_t n = (size_t)ctx->n_obs;
+  if (int r = d2h(ctx, points, ctx->obs_pts.p, n * 24)) return r;
+  if (int r = d2h(ctx, lab, ctx->obs_lab.p, n * 24)) return r;
+  if (labels)
+    if (int r = d2h(ctx, labels, ctx->obs_labels.p, n * 4)) return r;
+  if (src_px) {
+    if (ctx->obs_host_stale || ctx->h_obs_src.empty()) {
+      if (!ctx->obs_src.p) return fail(ctx, PX_E_ARG, "source pixels were not uploaded with this scene");
+      if (int r = d2h(ctx, src_px, ctx->obs_src.p, n * 8)) return r;
+    } else {
+      memcpy(src_px, ctx->h_obs_src.data(), n * 8);
+    }
+  }
+  CU(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 
@@ -774,6 +873,8 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
 
   // organised views: valid when every target is an index-ascending subset of the
   // uploaded scene's organised observed cloud
+  if (obs_index != nullptr && ctx->have_scene && ctx->organised)
+    if (int r = fetch_obs_host(ctx)) return r;
   bool org = obs_index != nullptr && ctx->have_scene && ctx->organised && !ctx->h_obs_src.empty();
   std::vector<TgtOrg> orgs((size_t)n_targets);
   std::vector<int32_t> tmap, tpix;
@@ -1379,6 +1480,88 @@ int px_search_upload(px_ctx* ctx, int64_t n, const int32_t* object_ids, const do
   }
   CU(cudaStreamSynchronize(ctx->stream));  // `slots` is stack-owned
   ctx->n_cand = n;
+  return 0;
+}
+
+int px_search_upload_lattice(px_ctx* ctx, int32_t mode3dof, int32_t n_objects, const px_lattice* objs,
+                             const double world_to_cam[12], int32_t w2c_vec_order, const double cam_to_world[12],
+                             const px_gicp_cfg* gicp, int32_t rank, int32_t world, int64_t* n_local_out) {
+  if (!ctx || n_objects < 0 || (n_objects && !objs) || world < 1 || rank < 0 || rank >= world)
+    return fail(ctx, PX_E_ARG, "px_search_upload_lattice: bad arguments");
+  if (mode3dof && (!world_to_cam || (gicp && !cam_to_world))) return fail(ctx, PX_E_ARG, "px_search_upload_lattice: extrinsics missing");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<LatticeObjDev> od((size_t)n_objects);
+  std::vector<double> rot, tr;
+  std::vector<int32_t> label_ids;
+  long long n_local = 0;
+  int n_targets = 0;
+  for (int o = 0; o < n_objects; ++o) {
+    const px_lattice& L = objs[o];
+    if (L.n_outer <= 0 || L.n_inner <= 0 || !L.rotations || !L.translations)
+      return fail(ctx, PX_E_ARG, "px_search_upload_lattice: empty lattice factor");
+    auto it = ctx->slot_of.find(L.object_id);
+    if (it == ctx->slot_of.end()) return fail(ctx, PX_E_ARG, "no model registered for id " + std::to_string(L.object_id));
+    LatticeObjDev& d = od[(size_t)o];
+    d.slot = it->second, d.n_outer = L.n_outer, d.n_inner = L.n_inner;
+    d.n_outer_local = L.n_outer > rank ? (L.n_outer - rank + world - 1) / world : 0;
+    d.cand_off = n_local;
+    d.rot_off = (long long)rot.size() / 9, d.tr_off = (long long)tr.size() / 3;
+    const int n_rot = mode3dof ? L.n_inner : L.n_outer, n_tr = mode3dof ? L.n_outer : L.n_inner;
+    rot.insert(rot.end(), L.rotations, L.rotations + 9 * (size_t)n_rot);
+    tr.insert(tr.end(), L.translations, L.translations + 3 * (size_t)n_tr);
+    d.z_lo = L.capsule[0], d.z_hi = L.capsule[1], d.radius = L.capsule[2];
+    d.tgt_off = n_targets, d.pad_ = 0;
+    if (d.n_outer_local > 0) {  // objects without a local candidate get no target (plan order: first appearance)
+      if (mode3dof) n_targets += d.n_outer_local;
+      else n_targets += 1, label_ids.push_back(L.object_id);
+    }
+    n_local += (long long)d.n_outer_local * L.n_inner;
+  }
+  if (n_local > 0x7fffffff) return fail(ctx, PX_E_LIMIT, "more than 2^31 candidates in one call");
+  const size_t n1 = (size_t)std::max<long long>(n_local, 1);
+  if (int r = h2d(ctx, ctx->lat_objs, od.data(), od.size() * sizeof(LatticeObjDev))) return r;
+  if (int r = h2d(ctx, ctx->lat_rot, rot.data(), rot.size() * 8)) return r;
+  if (int r = h2d(ctx, ctx->lat_tr, tr.data(), tr.size() * 8)) return r;
+  CU(ctx->c_slot.ensure(n1 * 4));
+  CU(ctx->c_pose.ensure(n1 * 96));
+  CU(ctx->c_rank.ensure(n1 * 4));
+  CU(ctx->c_tidx.ensure(n1 * 4));
+  const bool want_targets = gicp != nullptr;
+  if (want_targets && mode3dof) CU(ctx->tgt_params.ensure((size_t)std::max(n_targets, 1) * 40));
+  LatticeArgs a{};
+  a.mode3dof = mode3dof, a.n_objects = n_objects, a.rank = rank, a.world = world, a.n_local = n_local;
+  a.objs = ctx->lat_objs.as<LatticeObjDev>(), a.rotations = ctx->lat_rot.as<double>(), a.translations = ctx->lat_tr.as<double>();
+  if (mode3dof) memcpy(a.w2c, world_to_cam, sizeof a.w2c);
+  a.w2c_vec_order = w2c_vec_order;
+  a.slot = ctx->c_slot.as<int32_t>(), a.poses = ctx->c_pose.as<double>(), a.rank_in_object = ctx->c_rank.as<int32_t>();
+  a.tidx = want_targets ? ctx->c_tidx.as<int32_t>() : nullptr;
+  a.capsules = want_targets && mode3dof ? ctx->tgt_params.as<double>() : nullptr;
+  CU(launch_lattice(a, ctx->stream));
+  if (n_local) ctx->launches += 1;
+  CU(cudaStreamSynchronize(ctx->stream));  // od / rot / tr are stack-owned
+  ctx->n_cand = n_local;
+  ctx->have_tidx = want_targets;
+  ctx->tidx_max = want_targets ? n_targets - 1 : -1;
+  if (n_local_out) *n_local_out = n_local;
+  if (!want_targets) return 0;
+  if (mode3dof) {
+    TgtBuildArgs t{};
+    t.n_targets = n_targets, t.mode = 0, t.params = ctx->tgt_params.as<double>();
+    memcpy(t.c2w, cam_to_world, sizeof t.c2w);
+    return build_targets_device(ctx, t, gicp);
+  }
+  return px_targets_build_labels(ctx, (int32_t)label_ids.size(), label_ids.data(), gicp);
+}
+
+int px_search_candidates(px_ctx* ctx, int32_t* model_slot, double* poses, int32_t* target_idx, int32_t* rank_in_object) {
+  if (!ctx) return PX_E_ARG;
+  const size_t n = (size_t)ctx->n_cand;
+  if (int r = d2h(ctx, model_slot, ctx->c_slot.p, n * 4)) return r;
+  if (int r = d2h(ctx, poses, ctx->c_pose.p, n * 96)) return r;
+  if (target_idx && ctx->have_tidx)
+    if (int r = d2h(ctx, target_idx, ctx->c_tidx.p, n * 4)) return r;
+  if (int r = d2h(ctx, rank_in_object, ctx->c_rank.p, n * 4)) return r;
+  CU(cudaStreamSynchronize(ctx->stream));
   return 0;
 }
 

@@ -255,6 +255,56 @@ struct WinnerArgs {
 };
 cudaError_t launch_winners(const WinnerArgs& a, cudaStream_t st);
 
+// raster.frame_to_cloud + cloud_labels on the device (px_scene.cu)
+struct SceneCloudArgs {
+  int H, W, stride, GW, GH;
+  double fx, fy, cx, cy;
+  const double* depth;        // (H,W)
+  const uint8_t* valid;       // (H,W)
+  const int32_t* labels;      // (H,W)
+  const double* color_grid;   // (GH,GW,3) sRGB of the stride-grid pixels
+  long long* row_count;       // (GH) out of the count pass
+  const long long* row_offset;  // (GH) exclusive scan
+  double* pts;                // (n,3)
+  double* lab;                // (n,3)
+  int32_t* src;               // (n,2) (u,v)
+  int32_t* labels_out;        // (n)
+  int32_t* cell;              // (n)
+  double *gx, *gy, *gz;       // (GH*GW), NaN where no point
+  int32_t* gidx;              // (GH*GW), -1 where no point
+};
+cudaError_t launch_scene_count(const SceneCloudArgs& a, cudaStream_t st);
+cudaError_t launch_scene_fill(const SceneCloudArgs& a, cudaStream_t st);
+cudaError_t launch_label_count(const int32_t* labels, long long n, const ModelDev* models, int n_models, int32_t* out,
+                               cudaStream_t st);
+
+// candidate lattice of one search, generated on the device (px_scene.cu)
+struct LatticeObjDev {
+  int slot;               // model slot
+  int n_outer, n_inner;   // 3-DoF: cells x yaws; 6-DoF: rotations x translations
+  int n_outer_local;      // outer items owned by this rank
+  long long cand_off;     // first local candidate of the object
+  long long rot_off, tr_off;  // into LatticeArgs::rotations (units of 9) / translations (units of 3)
+  int tgt_off;            // 3-DoF: first local GICP target of the object; 6-DoF: the object's target
+  int pad_;
+  double z_lo, z_hi, radius;  // 3-DoF capsule of the per-cell target
+};
+struct LatticeArgs {
+  int mode3dof, n_objects, rank, world;
+  long long n_local;
+  const LatticeObjDev* objs;
+  const double* rotations;
+  const double* translations;
+  double w2c[12];
+  int w2c_vec_order;
+  int32_t* slot;            // (n_local) out
+  double* poses;            // (n_local,12) out
+  int32_t* rank_in_object;  // (n_local) out
+  int32_t* tidx;            // (n_local) out, nullable
+  double* capsules;         // (n_targets,5) out, nullable
+};
+cudaError_t launch_lattice(const LatticeArgs& a, cudaStream_t st);
+
 cudaError_t launch_ciede(const double* lab_a, const double* lab_b, double* out, long long n, cudaStream_t st);
 cudaError_t launch_lab(const double* rgb, double* out, long long n, int encode_first, cudaStream_t st);
 

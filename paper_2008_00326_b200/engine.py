@@ -91,6 +91,63 @@ class Engine:
         self._scene_key = key
         self._keep = [frame]
 
+    def upload_frame(self, frame, stride: int) -> int:
+        """Scene upload with the observed cloud built on the device (raster.frame_to_cloud + cloud_labels,
+        raster.py:191-217); returns the number of observed points."""
+        k = frame.intrinsics
+        depth = N.f64(frame.depth.values)
+        valid = np.ascontiguousarray(frame.depth.valid, dtype=np.uint8)
+        labels = N.i32(frame.labels)
+        cgrid = np.ascontiguousarray(frame.color[::stride, ::stride], dtype=np.float64)
+        intr = np.array([k.fx, k.fy, k.cx, k.cy], dtype=np.float64)
+        n = C.c_int64(0)
+        rc = self.lib.px_scene_upload_frame(self.ctx, k.height, k.width, N.ptr(depth, N.f64p), N.ptr(valid, N.u8p),
+                                            N.ptr(labels, N.i32p), N.ptr(cgrid, N.f64p), N.ptr(intr, N.f64p), int(stride),
+                                            C.cast(C.byref(n), N.i64p))
+        N.check(self.ctx, rc, "px_scene_upload_frame")
+        self._scene_key = None
+        self._keep = [frame]
+        return int(n.value)
+
+    def download_scene_cloud(self, n: int):
+        """(points, lab, source_pixel, labels) of the resident observed cloud."""
+        pts, lab = np.empty((n, 3)), np.empty((n, 3))
+        src, lbl = np.empty((n, 2), dtype=np.int32), np.empty(n, dtype=np.int32)
+        rc = self.lib.px_scene_download_cloud(self.ctx, N.ptr(pts, N.f64p), N.ptr(lab, N.f64p), N.ptr(src, N.i32p), N.ptr(lbl, N.i32p))
+        N.check(self.ctx, rc, "px_scene_download_cloud")
+        return pts, lab, src, lbl
+
+    def search_upload_lattice(self, plan, rank: int = 0, world: int = 1) -> int:
+        """Candidates (and GICP targets) of a lattice plan generated on the device; returns the local count."""
+        cfg = plan.cfg
+        arr = (N.Lattice * max(len(plan.lattice), 1))()
+        keep = []
+        for i, f in enumerate(plan.lattice):
+            r, t = N.f64(f.rotations), N.f64(f.translations)
+            keep += [r, t]
+            arr[i].object_id, arr[i].n_outer, arr[i].n_inner = int(f.object_id), int(f.n_outer), int(f.n_inner)
+            arr[i].rotations, arr[i].translations = N.ptr(r, N.f64p), N.ptr(t, N.f64p)
+            arr[i].capsule[:] = [float(x) for x in f.capsule]
+        w2c, c2w = N.f64(plan.w2c), N.f64(plan.c2w)
+        g = self._gicp_cfg(cfg.gicp)
+        n = C.c_int64(0)
+        rc = self.lib.px_search_upload_lattice(self.ctx, int(cfg.mode == "3dof"), len(plan.lattice), arr, N.ptr(w2c, N.f64p),
+                                               int(plan.w2c_vec_order), N.ptr(c2w, N.f64p),
+                                               C.byref(g) if cfg.refine else None, int(rank), int(world),
+                                               C.cast(C.byref(n), N.i64p))
+        N.check(self.ctx, rc, "px_search_upload_lattice")
+        return int(n.value)
+
+    def download_candidates(self, n: int, with_targets: bool = True):
+        slot, rank = np.zeros(n, dtype=np.int32), np.zeros(n, dtype=np.int32)
+        pose = np.empty((n, 3, 4))
+        tidx = np.zeros(n, dtype=np.int32) if with_targets else None
+        rc = self.lib.px_search_candidates(self.ctx, N.ptr(slot, N.i32p), N.ptr(pose, N.f64p), N.ptr(tidx, N.i32p), N.ptr(rank, N.i32p))
+        N.check(self.ctx, rc, "px_search_candidates")
+        ids = np.zeros(max(int(self.lib.px_model_count(self.ctx)), 1), dtype=np.int32)
+        self.lib.px_model_ids(self.ctx, N.ptr(ids, N.i32p))
+        return ids[slot], pose, tidx, rank
+
     def upload_model(self, object_id: int, mesh, cylinder=None):
         if mesh.num_triangles == 0:
             raise EmptyMesh("mesh has no triangles")

@@ -25,7 +25,7 @@ import numpy as np
 
 from .blas_probe import check_blas_orders
 from .cost import CostBreakdown, CostParams
-from .errors import ConfigError, EmptyBatch, NoValidDepth
+from .errors import ConfigError, EmptyBatch, NoValidDepth  # noqa: F401
 from .geometry import RigidTransform, rotation_angle
 from .model import LabeledCloud
 from .proposals import (PoseProposalSet, compose_grid, compose_many, grid_proposals_3dof,
@@ -212,10 +212,31 @@ class SearchPlan:
     c2w_vec_order: int = 0           # 0: rotation C-contiguous, 1: transposed view
     w2c_vec_order: int = 1
     cam_to_world: RigidTransform | None = None  # the frame's own object (its array layout decides numpy's rounding order)
+    # device-generated candidates (plan_lattice): per active object the outer x inner factors of its proposal set;
+    # the flat arrays above stay None and the observed cloud is built on the device
+    lattice: list | None = None      # [LatticeFactor]
+    n_observed: int | None = None
 
     @property
     def n(self) -> int:
+        if self.lattice is not None:
+            return int(sum(f.n_outer * f.n_inner for f in self.lattice))
         return int(self.flat_oid.shape[0])
+
+    def count_of(self, oid: int) -> int:
+        """Candidates of one object (ObjectEstimate.proposals_evaluated, search.py:365)."""
+        if self.lattice is not None:
+            return int(sum(f.n_outer * f.n_inner for f in self.lattice if f.object_id == oid))
+        return int(np.count_nonzero(self.flat_oid == oid))
+
+    def provenance_of(self, oid: int, local: int) -> tuple:
+        if self.lattice is not None:
+            f = next(f for f in self.lattice if f.object_id == oid)
+            return (int(local // f.n_inner), int(local % f.n_inner))
+        return tuple(int(x) for x in self.proposal_sets[oid].provenance[local])
+
+    def observed_count(self) -> int:
+        return int(self.n_observed) if self.n_observed is not None else len(self.observed)
 
     def rank_in_object(self) -> np.ndarray:
         """Position of each candidate among its object's candidates: the index
@@ -229,6 +250,19 @@ class SearchPlan:
             rank[sel] = np.arange(sel.size, dtype=np.int32)
         self._rank_cache = rank
         return rank
+
+
+@dataclass
+class LatticeFactor:
+    """One object's proposal set as an outer x inner product (proposals.py:163-210): 3-DoF outer = grid cells
+    (translations), inner = yaw spins (rotations); 6-DoF outer = rotations, inner = translations."""
+
+    object_id: int
+    n_outer: int
+    n_inner: int
+    rotations: np.ndarray      # (n_inner,3,3) in 3-DoF, (n_outer,3,3) in 6-DoF
+    translations: np.ndarray   # (n_outer,3) in 3-DoF, (n_inner,3) in 6-DoF
+    capsule: tuple = (0.0, 0.0, 0.0)  # 3-DoF GICP target capsule: z_lo, z_hi, radius (search.py:407-426)
 
 
 def _capsule_mask(pw, x, y, z_lo, z_hi, radius):
@@ -316,6 +350,62 @@ def plan_search(frame, models: dict, cfg: SearchConfig, build_targets: bool = Tr
     if cfg.refine and build_targets and plan.n:
         _plan_targets(plan, models, cam_to_world, materialise_targets)
     return plan
+
+
+def plan_lattice(frame, models: dict, cfg: SearchConfig) -> SearchPlan | None:
+    """The per-scene plan for device-side set-up (SURVEY 8(f) ranks 1 + 2): proposal FACTORS per object instead of
+    per-candidate arrays -- the device forms every candidate's camera pose (px_search_upload_lattice) and builds
+    the observed cloud from the frame (px_scene_upload_frame).  None when the configuration needs the flat host
+    plan (`max_proposals` subsampling picks arbitrary candidates, search.py:259-265)."""
+    if cfg.max_proposals is not None:
+        return None
+    check_blas_orders()
+    k = frame.intrinsics
+    cam_to_world = RigidTransform(k.camera_pose.rotation, k.camera_pose.translation)
+    world_to_cam = cam_to_world.inverse()
+    object_ids = [d.object_id for d in frame.detections] if frame.detections else sorted(models)
+    if cfg.mode == "6dof" and not frame.detections:
+        raise ConfigError("6dof mode requires detections in the frame")
+    failures, factors = {}, []
+    grid = None
+    for oid in object_ids:
+        if oid not in models:
+            failures[oid] = "unknown_object"
+            continue
+        m = models[oid]
+        if cfg.mode == "3dof":
+            from .proposals import lattice_3dof
+            if grid is None:
+                grid = {}
+            key = bool(m.yaw_symmetric)
+            if key not in grid:
+                grid[key] = lattice_3dof(cfg.workspace, cfg.dt, cfg.dyaw, cfg.fixed_z, key)
+            cells, spins = grid[key]
+            cyl = m.inscribed_cylinder
+            cap = (cfg.fixed_z + cyl.z_min + 0.005, cfg.fixed_z + cyl.z_max, 1.5 * cyl.radius + cfg.dt)
+            if cells.shape[0] == 0:
+                failures[oid] = "empty_proposal_set"
+                continue
+            factors.append(LatticeFactor(oid, cells.shape[0], spins.shape[0], spins, cells, cap))
+        else:
+            try:
+                det = next(d for d in frame.detections if d.object_id == oid)
+                rot = rotation_proposals(cfg.viewpoints, 1 if m.yaw_symmetric else cfg.n_inplane)
+                tr = translation_proposals(det, frame.depth, frame.labels, frame.intrinsics, cfg.z_step)
+            except NoValidDepth:
+                failures[oid] = "no_valid_depth"
+                continue
+            if len(rot) == 0 or len(tr) == 0:
+                failures[oid] = "empty_proposal_set"
+                continue
+            factors.append(LatticeFactor(oid, len(rot), len(tr), rot.rotations, tr.translations))
+    active = [f.object_id for f in factors]
+    return SearchPlan(cfg, object_ids, failures, active, {}, None, None, None, None, None,
+                      c2w=np.ascontiguousarray(cam_to_world.matrix3x4()),
+                      w2c=np.ascontiguousarray(world_to_cam.matrix3x4()),
+                      c2w_vec_order=_vec_order(cam_to_world.rotation),
+                      w2c_vec_order=_vec_order(world_to_cam.rotation),
+                      cam_to_world=cam_to_world, lattice=factors)
 
 
 def _plan_targets(plan: SearchPlan, models, cam_to_world, materialise: bool = True) -> None:
@@ -420,18 +510,17 @@ def _assemble(plan: SearchPlan, winners: dict, stage_millis: dict, t_start: floa
             continue
         key, refined, reg_T, j_o, j_r = winners[oid]
         best_local = key & 0xFFFFFFFF
-        n_obj = int(np.count_nonzero(plan.flat_oid == oid))
-        pset = plan.proposal_sets[oid]
+        n_obj = plan.count_of(oid)
         world = c2w.compose(RigidTransform.from_matrix3x4(refined))
         delta = RigidTransform.from_matrix3x4(reg_T)
         share = per_stage_total * (n_obj / max(1, plan.n))
         estimates.append(ObjectEstimate(
             oid, world, CostBreakdown(j_o=j_o, j_r=j_r),
-            tuple(int(x) for x in pset.provenance[best_local]), best_local,
+            plan.provenance_of(oid, best_local), best_local,
             float(np.linalg.norm(delta.translation)), rotation_angle(delta.rotation),
             n_obj, share))
     total_millis = (time.perf_counter() - t_start) * 1e3
-    return SearchResult(tuple(estimates), stage_millis, total_millis, plan.n, max_pts, len(plan.observed))
+    return SearchResult(tuple(estimates), stage_millis, total_millis, plan.n, max_pts, plan.observed_count())
 
 
 def assemble_result(plan: SearchPlan, out: StageOutputs, t_start: float) -> SearchResult:
@@ -485,7 +574,12 @@ def estimate_poses_distributed(frame, models: dict, cfg: SearchConfig, runner=No
         eng = default_engine()
         if eng.comm_world() != world:
             eng.comm_init_torch()
-        winners, stage_millis, max_pts = _device_search(eng, frame, models, plan, idx)
+        lat = plan_lattice(frame, models, cfg)
+        if lat is not None and lat.n:
+            plan = lat
+            winners, stage_millis, max_pts = _device_search(eng, frame, models, plan, (rank, world))
+        else:
+            winners, stage_millis, max_pts = _device_search(eng, frame, models, plan, idx)
         t = torch.tensor([stage_millis[k] for k in ("render", "refine", "rerender", "cost")], dtype=torch.float64,
                          device=torch.device("cuda", eng.device))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)  # stage times: slowest rank
@@ -523,9 +617,16 @@ def estimate_poses_distributed(frame, models: dict, cfg: SearchConfig, runner=No
 
 def _device_search(eng, frame, models, plan: SearchPlan, index=None):
     """Upload, fused search, on-device argmin (+ NCCL reduction when a communicator is up); only the
-    per-object winner records come back to the host.  -> (winners, stage_millis, max_rendered_points)."""
-    eng.prepare_plan(frame, models, plan)
-    eng.search_upload(plan, index)
+    per-object winner records come back to the host.  -> (winners, stage_millis, max_rendered_points).
+    `index`: candidate subset of a flat plan, or (rank, world) for a lattice plan (the device generates the shard)."""
+    if plan.lattice is not None:
+        rank, world = index if index is not None else (0, 1)
+        plan.n_observed = eng.upload_frame(frame, plan.cfg.stride)
+        eng.upload_models({oid: models[oid] for oid in plan.active})
+        eng.search_upload_lattice(plan, rank, world)
+    else:
+        eng.prepare_plan(frame, models, plan)
+        eng.search_upload(plan, index)
     eng.search_run(eng.search_cfg(plan))
     eng.search_reduce()
     win = eng.search_winners()
@@ -545,6 +646,13 @@ def estimate_poses(frame, models: dict, cfg: SearchConfig) -> SearchResult:
     except ImportError:
         pass
     t_start = time.perf_counter()
+    if not cfg.trace_path:
+        plan = plan_lattice(frame, models, cfg)  # candidates, observed cloud and targets are built on the device
+        if plan is not None and plan.n:
+            winners, stage_millis, max_pts = _device_search(default_engine(), frame, models, plan)
+            sm = {"render": 0.0, "refine": 0.0, "rerender": 0.0, "cost": 0.0}
+            sm.update(stage_millis)
+            return _assemble(plan, winners, sm, t_start, max_pts)
     plan = plan_search(frame, models, cfg, materialise_targets=False)  # the device crops the GICP targets
     if plan.n == 0:
         out = StageOutputs(np.zeros((0, 3, 4)), np.zeros((0, 3, 4)), np.zeros(0, np.int32),

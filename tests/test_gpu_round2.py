@@ -200,3 +200,75 @@ def test_knife_edge_log(engine):
     assert 0.0 < k["min_abs_d2_minus_delta2"] < cfg.delta ** 2
     assert k["min_abs_dE_minus_tau_c"] > 1e-9
     print("knife edges:", k)
+
+
+# ---- per-scene set-up on the device -------------------------------------
+
+@pytest.mark.parametrize("name", ["c1_box_3dof", "c2_twocyl_color1", "c3n_clutter_noisy", "c4_mixed_6dof"])
+def test_device_observed_cloud_equals_host(engine, name):
+    """raster.frame_to_cloud + cloud_labels on the device (px_scene_upload_frame): points, source pixels,
+    order and labels bit-identical to the host path (itself pinned to the reference by
+    tests/test_oracle_golden.py), Lab to 1e-9 (libdevice pow / cbrt)."""
+    d, frame, models, cfg, plan = G.scene(name)
+    n = engine.upload_frame(frame, cfg.stride)
+    assert n == len(plan.observed) == int(d["n_obs"])
+    pts, lab, src, lbl = engine.download_scene_cloud(n)
+    assert np.array_equal(pts, plan.observed.points) and np.array_equal(src, plan.observed.source_pixel)
+    assert np.array_equal(lbl, plan.obs_labels)
+    assert np.abs(lab - plan.observed.lab_colors).max() < 1e-9
+
+
+def _lattice_cfgs():
+    out = []
+    for name, over in (("c1_box_3dof", {}), ("c2_twocyl_color1", {}), ("c3_clutter_3dof", dict(dt=0.08, max_proposals=None)),
+                       ("c4_mixed_6dof", dict(viewpoints=12, n_inplane=4, max_proposals=None))):
+        out.append((name, over))
+    return out
+
+
+@pytest.mark.parametrize("name,over", _lattice_cfgs())
+def test_device_lattice_equals_host_plan(engine, name, over):
+    """Candidate generation + pose composition on the device (px_search_upload_lattice) against the host plan
+    (proposals.compose_grid, bit-equal to the reference's per-candidate world_to_cam.compose(pose_i),
+    search.py:253-257): object ids, camera poses, target indices, ranks -- and the device-built targets --
+    are bit-identical; a rank's shard equals dist.shard_index."""
+    from paper_2008_00326_b200 import dist as pxd
+    from paper_2008_00326_b200.search import plan_lattice
+    d, frame, models, cfg, _ = G.scene(name)
+    cfg = dataclasses.replace(cfg, **over)
+    host = plan_search(frame, models, cfg)
+    lat = plan_lattice(frame, models, cfg)
+    assert lat is not None and lat.n == host.n and lat.active == host.active
+    engine.upload_frame(frame, cfg.stride)
+    engine.upload_models({o: models[o] for o in lat.active})
+    n = engine.search_upload_lattice(lat, 0, 1)
+    assert n == host.n
+    oid, pose, tidx, rank = engine.download_candidates(n, cfg.refine)
+    assert np.array_equal(oid, host.flat_oid) and np.array_equal(rank, host.rank_in_object())
+    assert np.array_equal(pose, host.cam_poses)
+    if cfg.refine:
+        assert np.array_equal(tidx, host.target_idx)
+        off, pts, oi = engine.download_targets()
+        assert np.array_equal(off, host.target_offsets) and np.array_equal(pts, host.target_points)
+    for r in range(3):   # the shard of rank r of 3
+        idx = pxd.shard_index(host, r, 3)
+        n_r = engine.search_upload_lattice(lat, r, 3)
+        assert n_r == idx.size
+        oid, pose, tidx, rank = engine.download_candidates(n_r, cfg.refine)
+        assert np.array_equal(oid, host.flat_oid[idx]) and np.array_equal(pose, host.cam_poses[idx])
+        assert np.array_equal(rank, host.rank_in_object()[idx])
+
+
+@pytest.mark.parametrize("name,over", _lattice_cfgs())
+def test_estimate_poses_device_setup_equals_flat_plan(engine, name, over):
+    """The public call with everything per-scene built on the device (observed cloud + Lab, candidates, targets)
+    returns byte-identical result JSON to the host-planned flat path."""
+    from paper_2008_00326_b200 import estimate_poses
+    d, frame, models, cfg, _ = G.scene(name)
+    cfg = dataclasses.replace(cfg, **over)
+    res = estimate_poses(frame, models, cfg)
+    host = plan_search(frame, models, cfg)
+    full = assemble_result(host, engine.run_plan(frame, models, host), 0.0)
+    assert result_to_json(res) == result_to_json(full)
+    assert (res.max_rendered_points, res.observed_points, res.proposals_evaluated) == \
+           (full.max_rendered_points, full.observed_points, full.proposals_evaluated)
