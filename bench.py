@@ -258,13 +258,20 @@ def run_gpu(args):
 
     # ---- end-to-end arm (`e2e`): host buffers -> C-ABI -> host results, every step ----
     barrier()
+    from paper_2008_00326_b200.search import plan_lattice
+    lat = plan_lattice(frame, models, cfg)   # proposal factors (host, per scene); None: flat candidate upload
     e2e_ms = []
     for s in range(max(2, min(args.steps, 5)) + 1):
         t0 = time.perf_counter()
         eng._scene_key = None
         eng._model_keys.clear()
-        eng.prepare_plan(frame, models, plan)
-        eng.search_upload(plan, idx)
+        if lat is not None:
+            eng.upload_frame(frame, cfg.stride)            # frame planes from host memory; observed cloud on the device
+            eng.upload_models({o: models[o] for o in lat.active})
+            eng.search_upload_lattice(lat, rank, world)    # proposal factors from host memory; candidates + targets on the device
+        else:
+            eng.prepare_plan(frame, models, plan)
+            eng.search_upload(plan, idx)
         eng.search_run(sc)
         eng.search_reduce()
         wins, wkeys = winners_keys()   # device -> host read of the step's result (per-object winner records)
@@ -275,9 +282,12 @@ def run_gpu(args):
     k_ = frame.intrinsics
     npix = k_.width * k_.height
     n_specs = 0 if plan.target_idx is None else int(plan.target_idx.max()) + 1
-    h2d = (npix * 13 + len(plan.observed) * (24 + 24 + 8 + 4) + n_specs * 40
-           + sum(m.mesh.vertices.size * 16 + m.mesh.triangles.size * 4 for m in models.values())
-           + n_local * (96 + 12))
+    model_bytes = sum(m.mesh.vertices.size * 16 + m.mesh.triangles.size * 4 for m in models.values())
+    if lat is not None:
+        ng = ((k_.width + cfg.stride - 1) // cfg.stride) * ((k_.height + cfg.stride - 1) // cfg.stride)
+        h2d = npix * 13 + ng * 24 + model_bytes + sum(f.rotations.size * 8 + f.translations.size * 8 + 64 for f in lat.lattice)
+    else:
+        h2d = npix * 13 + len(plan.observed) * (24 + 24 + 8 + 4) + n_specs * 40 + model_bytes + n_local * (96 + 12)
     d2h = 8 * 28 * len(models) + 32
     e2e_t = float(np.median(e2e_ms)) * 1e-3
     if world > 1:
@@ -360,6 +370,11 @@ def run_gpu(args):
                 "whole_step_frac": ab["total"] / (ms_per_step * 1e-3) / 1e9 / hbm_peak,
                 "bytes_per_candidate": ab["total"] / max(n_local, 1)}
 
+    # ---- per-scene latency and multi-scene batching on the small config (BASELINE: "per-scene latency") ----
+    latency = None
+    if world == 1 and not args.no_latency:
+        latency = small_scene_latency(eng)
+
     # ---- CPU baseline on a bounded sample of the same workload (rank 0, N=1 only) ----
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -381,12 +396,14 @@ def run_gpu(args):
         "knife_edges": knife,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_t * 1e3,
-                "path": "scene + models + GICP target specs + candidates from host buffers -> C-ABI (targets cropped on the "
-                        "device, argmin + winner records reduced on the device) -> per-object results on the host",
+                "path": ("frame planes + models + proposal factors from host buffers -> C-ABI (observed cloud, candidate poses, "
+                         "GICP targets built on the device; argmin + winner records reduced on the device) -> per-object "
+                         "results on the host") if lat is not None else
+                        ("scene + models + GICP target specs + candidates from host buffers -> C-ABI -> per-object results on the host"),
                 "estimate_poses_ms": api_ms,
                 "estimate_poses_value": (n_total / (api_ms * 1e-3)) if api_ms else None},
         "gpu_launches": int(launches),
-        "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "latency": latency,
         "mean_iterations": float(full.iterations.mean()), "mean_rendered_points": float(full.n_rendered.mean()),
     }
     print(json.dumps(line))
@@ -394,6 +411,37 @@ def run_gpu(args):
         eng.lib.px_comm_destroy(eng.ctx)
     if world > 1:
         dist.destroy_process_group()
+
+
+def small_scene_latency(eng, scenes: int = 16, streams: int = 4):
+    """BASELINE configs[0] (C1: one box, 1,936 candidates, GICP on): milliseconds of the public call for one scene
+    (host planning + frame upload + device set-up + search + argmin + result on the host), and throughput with
+    several scenes in flight (batch.estimate_poses_many: one device context / CUDA stream per scene in flight)."""
+    import golden_io as G
+    from paper_2008_00326_b200 import estimate_poses, estimate_poses_many
+
+    d = G.load("c1_box_3dof")
+    frame, models, cfg = G.frame_of(d), G.models_of(d), G.config_of(d)
+    ts = []
+    for i in range(8):
+        t0 = time.perf_counter()
+        res = estimate_poses(frame, models, cfg, engine=eng)
+        if i >= 3:
+            ts.append((time.perf_counter() - t0) * 1e3)
+    jobs = [(frame, models, cfg)] * scenes
+    estimate_poses_many(jobs[:streams], streams=streams)  # contexts created, kernels loaded
+    t0 = time.perf_counter()
+    estimate_poses_many(jobs, streams=streams)
+    many_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    estimate_poses_many(jobs, streams=1)
+    one_s = time.perf_counter() - t0
+    n = res.proposals_evaluated
+    return {"workload": "c1: c1_box_3dof scene, mode=3dof, refine=True, 1,936 candidates, 640x480",
+            "estimate_poses_ms": float(np.median(ts)), "stage_ms": res.stage_millis,
+            "multi_scene": {"scenes": scenes, "streams": streams, "ms_per_scene": many_s / scenes * 1e3,
+                            "poses_per_s": n * scenes / many_s, "ms_per_scene_one_stream": one_s / scenes * 1e3,
+                            "poses_per_s_one_stream": n * scenes / one_s}}
 
 
 def sample_groups(plan, idx, sample: int) -> np.ndarray:
@@ -537,6 +585,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=None,
                     help="candidates in the bounded CPU sample (default 40000 for cpu_baseline, 20000 per --impl reference step)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-latency", action="store_true", help="skip the small-scene latency / multi-scene section")
     ap.add_argument("--scale", type=int, default=1, help="refine the yaw/viewpoint axis: candidates x scale (C5 sweep)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup

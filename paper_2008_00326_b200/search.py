@@ -635,9 +635,13 @@ def _device_search(eng, frame, models, plan: SearchPlan, index=None):
     return winners, eng.stage_millis(), max_pts
 
 
-def estimate_poses(frame, models: dict, cfg: SearchConfig) -> SearchResult:
-    """Estimate a pose for every detected object (search.py:217-377)."""
-    from .engine import default_engine
+def estimate_poses(frame, models: dict, cfg: SearchConfig, engine=None) -> SearchResult:
+    """Estimate a pose for every detected object (search.py:217-377).  `engine` (optional, not in the
+    reference's signature) selects the device context; default: the process-wide one."""
+    from .engine import default_engine as _default_engine
+
+    def default_engine():
+        return engine if engine is not None else _default_engine()
 
     try:
         import torch.distributed as dist
