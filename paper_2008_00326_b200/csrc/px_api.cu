@@ -90,6 +90,7 @@ struct px_ctx {
   DevBuf tgt_v0, tgt_obs, tgt_world, tgt_sizes, tgt_scans, tgt_params,
          tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
   bool tgt_organised = false;
+  double tgt_rot[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // TargetsDev::rot of the resident targets
   bool tgt_obs_valid = false;  // tgt_obs holds the observed indices of the resident targets (device-built)
   // resident candidates
   int64_t n_cand = 0;
@@ -849,6 +850,7 @@ static TargetsDev targets_dev(px_ctx* ctx) {
   t.soa = ctx->tgt_soa.as<double>();
   t.plane = std::max<long long>(ctx->tgt_total, 1);
   t.f = 1.0 - ctx->tgt_eps;
+  memcpy(t.rot, ctx->tgt_rot, sizeof t.rot);
   return t;
 }
 
@@ -1019,6 +1021,10 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     }
   }
   ctx->tgt_organised = org, ctx->tgt_obs_valid = false;
+  {
+    const double I9[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // host-built structures are in the camera frame
+    memcpy(ctx->tgt_rot, I9, sizeof I9);
+  }
 
   if (int r = h2d(ctx, ctx->tgt_off, off.data(), off.size() * 8)) return r;
   if (int r = h2d(ctx, ctx->tgt_pts, points, (size_t)total * 24)) return r;
@@ -1066,6 +1072,26 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   a.obs_cell = ctx->obs_cell.as<int32_t>(), a.gidx = ctx->gidx.as<int32_t>(), a.n_obs = ctx->n_obs, a.GW = ctx->cam.GW;
   a.world = ctx->tgt_world.as<double>();
   a.gate = cfg->max_correspondence_distance;
+  {
+    // frame of the fp32 pruning structures: in 3-DoF the world frame, where the supporting plane (most of every
+    // capsule crop) is axis-aligned; re-orthonormalised here (Gram-Schmidt in fp64) because the error bound of the
+    // pruning tests assumes an isometry.  6-DoF label sub-clouds have no common plane: identity.
+    double F[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    if (a.mode == 0 && n) {
+      double r0[3] = {a.c2w[0], a.c2w[1], a.c2w[2]}, r1[3] = {a.c2w[4], a.c2w[5], a.c2w[6]};
+      const double n0 = std::sqrt(r0[0] * r0[0] + r0[1] * r0[1] + r0[2] * r0[2]);
+      for (double& v : r0) v /= n0;
+      const double d01 = r0[0] * r1[0] + r0[1] * r1[1] + r0[2] * r1[2];
+      for (int q = 0; q < 3; ++q) r1[q] -= d01 * r0[q];
+      const double n1_ = std::sqrt(r1[0] * r1[0] + r1[1] * r1[1] + r1[2] * r1[2]);
+      for (double& v : r1) v /= n1_;
+      const double r2[3] = {r0[1] * r1[2] - r0[2] * r1[1], r0[2] * r1[0] - r0[0] * r1[2], r0[0] * r1[1] - r0[1] * r1[0]};
+      if (std::isfinite(n0) && std::isfinite(n1_) && n0 > 0.5 && n1_ > 0.5)
+        for (int q = 0; q < 3; ++q) F[q] = r0[q], F[3 + q] = r1[q], F[6 + q] = r2[q];
+    }
+    memcpy(a.frame, F, sizeof F);
+    memcpy(ctx->tgt_rot, F, sizeof F);
+  }
   a.cnt = ctx->tgt_sizes.as<long long>(), a.cells = a.cnt + n1, a.nodes = a.cells + n1;
   long long* off = ctx->tgt_off.as<long long>();
   long long* coff = ctx->tgt_scans.as<long long>();

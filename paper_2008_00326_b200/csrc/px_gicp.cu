@@ -432,7 +432,10 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
 #ifdef PX_NN_STATS
     int n_leaves_ = 0, n_improved_ = 0;
 #endif
-    const float qxf = (float)qx, qyf = (float)qy, qzf = (float)qz;
+    // the query in the frame of the fp32 structures (TargetsDev::rot; the exact evaluations below stay in the original frame)
+    const float qxf = (float)(T.rot[0] * qx + T.rot[1] * qy + T.rot[2] * qz);
+    const float qyf = (float)(T.rot[3] * qx + T.rot[4] * qy + T.rot[5] * qz);
+    const float qzf = (float)(T.rot[6] * qx + T.rot[7] * qy + T.rot[8] * qz);
     const int32_t* lstart = T.leaf_start + o.box_off + ti;  // (bw*bh + 1) entries per target
     const float4* lp = T.leaf32 + toff;                     // points grouped by block: {x, y, z, index bits}
     // boxes: per super-block six planes {cx,cy,cz,hx,hy,hz} x 16 block slots, then the super-blocks' {c,h}

@@ -110,6 +110,13 @@ struct TargetsDev {
   const double* soa;          // 6 planes of `plane` doubles: x, y, z and the normal v0 the covariance I - f v0 v0^T is
   long long plane;            //   made of -- coherent-gather copy for the linearise kernel, which rebuilds the matrix
   double f;                   // 1 - epsilon the target covariances were built with
+  // Frame of the fp32 pruning structures (boxes32, leaf32): x' = rot * x.  Axis-aligned boxes of a tilted plane are
+  // fat (a 4x4-cell patch of a table seen at 60 degrees of incidence is 1.9 x 1.9 x 3.3 cm in the camera frame, and
+  // its corners reach 1.6 cm off the plane); in a frame with the dominant plane axis-aligned they are thin, so their
+  // distance to a query is close to the true distance and far fewer blocks / leaves are opened.  The rotation only
+  // moves the conservative fp32 filter -- every surviving point is still evaluated in fp64 on the ORIGINAL
+  // coordinates -- so results do not depend on it.  Identity unless the builder knows better (3-DoF: camera -> world).
+  double rot[9];
 };
 
 // Device-side construction of GICP targets as subsets of the uploaded organised observed cloud
@@ -121,6 +128,7 @@ struct TgtBuildArgs {
   const int32_t* label_ids;   // mode 1: (n) object ids
   double c2w[12];             // camera -> world (mode 0)
   double gate;                // max_correspondence_distance (enters the fp32 pruning error bound)
+  double frame[9];            // TargetsDev::rot: frame of the fp32 pruning structures
   // scene
   const double* obs_pts;      // (n_obs,3) camera frame
   const int32_t* obs_labels;  // (n_obs)

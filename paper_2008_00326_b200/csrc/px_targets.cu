@@ -80,6 +80,11 @@ __global__ void tgt_offsets_kernel(TgtBuildArgs a) {
   a.org[t].box_off = a.nodes_off[t];
 }
 
+// coordinates in the frame of the fp32 pruning structures (TargetsDev::rot)
+__device__ __forceinline__ void to_frame(const double* __restrict__ F, double x, double y, double z, double* o) {
+  o[0] = F[0] * x + F[1] * y + F[2] * z, o[1] = F[3] * x + F[4] * y + F[5] * z, o[2] = F[6] * x + F[7] * y + F[8] * z;
+}
+
 // pass 2: ordered compaction -> obs index, points, map cell of every member; pixel map; error bound
 __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
   const int t = blockIdx.x;
@@ -116,7 +121,9 @@ __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
       a.tgt_pts[3 * (off + pos)] = x, a.tgt_pts[3 * (off + pos) + 1] = y, a.tgt_pts[3 * (off + pos) + 2] = z;
       a.tpix[off + pos] = lc;
       a.tmap[o.map_off + lc] = pos;
-      m = fmax(m, fmax(fabs(x), fmax(fabs(y), fabs(z))));
+      double f[3];
+      to_frame(a.frame, x, y, z, f);
+      m = fmax(m, fmax(fabs(f[0]), fmax(fabs(f[1]), fabs(f[2]))));
     }
     run += all;
     __syncthreads();
@@ -174,8 +181,10 @@ __global__ void __launch_bounds__(256) tgt_tree_kernel(TgtBuildArgs a) {
           const int j = map[y * o.w + x];
           if (j < 0) continue;
           ++cnt;
+          double f[3];
+          to_frame(a.frame, P[3 * j], P[3 * j + 1], P[3 * j + 2], f);
 #pragma unroll
-          for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], P[3 * j + d]), hi[d] = fmax(hi[d], P[3 * j + d]);
+          for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], f[d]), hi[d] = fmax(hi[d], f[d]);
         }
     if (sup) {
       float* o6 = bb + 96 * (size_t)ns + 6 * (size_t)s_;
@@ -217,7 +226,9 @@ __global__ void __launch_bounds__(256) tgt_tree_kernel(TgtBuildArgs a) {
       for (int x = cx0; x < min(cx0 + PX_BLK, o.w); ++x) {
         const int j = map[y * o.w + x];
         if (j < 0) continue;
-        lp[k++] = make_float4((float)P[3 * j], (float)P[3 * j + 1], (float)P[3 * j + 2], __int_as_float(j));
+        double f[3];
+        to_frame(a.frame, P[3 * j], P[3 * j + 1], P[3 * j + 2], f);
+        lp[k++] = make_float4((float)f[0], (float)f[1], (float)f[2], __int_as_float(j));
       }
   }
 }
