@@ -16,7 +16,7 @@ ap.add_argument("--scale", type=int, default=1)
 a = ap.parse_args()
 from paper_2008_00326_b200.engine import Engine  # noqa: E402
 
-frame, models, cfg, plan = bench.build_workload(a.workload, 1, a.scale)
+frame, models, cfg, plan = bench.build_workload(a.workload, 1, a.scale, materialise_targets=False)  # targets cropped on the device, as estimate_poses does
 eng = Engine(0)
 eng.prepare_plan(frame, models, plan)
 eng.set_kernel_timing(True)
