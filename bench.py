@@ -133,14 +133,14 @@ def algorithmic_bytes(plan_n, models, flat_oid, out, ncorr_sum, cap0, cap1, refi
          "refine": float((b_cov + b_iter_sum).sum()) if refine else 0.0, "cost": float(b_cost.sum())}
     d["total"] = sum(d.values())
     # the refine stage per kernel (B_iter = 104 n_r + 96 n_c + 344 split by which kernel consumes the operand:
-    # nn: source points in, correspondence out, matched target point; lin: source covariances, matched target
-    # point + covariance... the target point is charged to nn, its covariance to lin; halve re-reads operands
-    # the model already charged once, so its algorithmic bytes are 0)
+    # nn: source points in, correspondence out, matched target point; step (linearise + solve + halving, fused):
+    # source covariances, matched target covariance, H/g/f0 out; the halving re-reads operands the model already
+    # charged once, so it adds no algorithmic bytes)
     nc = ncorr_sum.astype(np.float64)
     d["kernels"] = {
         "gicp_init_kernel": float(b_cov.sum()) if refine else 0.0,
         "gicp_nn_kernel": float((it * 32 * n0 + 24 * nc).sum()) if refine else 0.0,
-        "gicp_lin_kernel": float((it * (72 * n0 + 344) + 72 * nc).sum()) if refine else 0.0,
+        "gicp_step_kernel": float((it * (72 * n0 + 344) + 72 * nc).sum()) if refine else 0.0,
         "gicp_halve_kernel": 0.0, "gicp_finish_kernel": 0.0,
     }
     return d
@@ -343,7 +343,7 @@ def run_gpu(args):
         traffic_db = json.loads(tj.read_text()).get(args.workload, {})
     table = {}
     for k, (ms, nl) in kern.items():
-        if nl <= 0:
+        if nl <= 0 or (k == "gicp_halve_kernel" and ms < 0.5):  # fused build: the halving runs inside gicp_step_kernel
             continue
         per_launch_ms, per_launch_b = ms / nl, kbytes.get(k, 0.0) / nl
         table[k] = {"launches_per_step": nl, "ms_per_step": ms, "ms_per_launch": per_launch_ms,

@@ -276,9 +276,10 @@ int px_search_knife_edges(px_ctx* ctx, double margins[2]);
 /* Per-kernel timing of the GICP stage (bench.py's roofline).  When switched on, px_search_run brackets
  * every launch of the refine stage with CUDA events on the context stream; px_search_kernel_ms then
  * returns, for the last run, total milliseconds and launch counts of
- * {gicp_init, gicp_nn, gicp_lin, gicp_halve, gicp_finish} (registration.py:500-511 per candidate:
- * source covariances; :251-261 nearest neighbours; :262-338 + :479-494 linearise and solve;
- * :443-471 step halving; :473 + search.py:291-301 result and refine-apply). */
+ * {gicp_init, gicp_nn, gicp_step, gicp_halve, gicp_finish} (registration.py:500-511 per candidate:
+ * source covariances; :251-261 nearest neighbours; :262-338 + :479-494 + :443-471 linearise, solve and
+ * step halving, fused in gicp_step_kernel -- the fourth slot is only used by -DPX_GICP_SPLIT builds, which
+ * run the halving as its own kernel; :473 + search.py:291-301 result and refine-apply). */
 int px_ctx_set_kernel_timing(px_ctx* ctx, int32_t on);
 int px_search_kernel_ms(px_ctx* ctx, double ms[5], int64_t launches[5]);
 /* Number of models uploaded and their ids in slot order (for best_key_per_model). */

@@ -1157,6 +1157,383 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
   }
 }
 
+// solve6 / solve_normal_equations with the six rows of the augmented system [H + diag | g] in lanes 0..5 (row i in
+// lane i): pivot search, row exchange, elimination and back-substitution perform exactly the operations of the scalar
+// routine (same operands, same order per element), so the result has the same bits; every lane returns x.
+__device__ __forceinline__ int warp_solve6(const double* __restrict__ h, double diag_add, const double* __restrict__ g,
+                                           double* __restrict__ x, int lane) {
+  const int row_id = lane < 6 ? lane : 5;
+  double row[7];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) row[j] = h[6 * row_id + j] + (row_id == j ? diag_add : 0.0);
+  row[6] = g[row_id];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    const double mine = fabs(row[c]);
+    int p = c;
+    double best = shfl_d(mine, c);
+#pragma unroll
+    for (int i = c + 1; i < 6; ++i) {
+      const double v = shfl_d(mine, i);
+      if (v > best) best = v, p = i;
+    }
+    if (best == 0.0 || isnan(best)) return 1;
+#pragma unroll
+    for (int j = c; j < 7; ++j) {  // exchange rows c and p (columns left of c are never read again)
+      const double vc = shfl_d(row[j], c), vp = shfl_d(row[j], p);
+      if (p != c) {
+        if (lane == c) row[j] = vp;
+        else if (lane == p) row[j] = vc;
+      }
+    }
+    const double inv = 1.0 / shfl_d(row[c], c);
+    const double l = row[c] * inv;
+#pragma unroll
+    for (int j = c + 1; j < 7; ++j) {
+      const double pv = shfl_d(row[j], c);
+      if (lane > c && lane < 6) row[j] = row[j] - l * pv;
+    }
+  }
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    double s_ = row[6];
+#pragma unroll
+    for (int j = i + 1; j < 6; ++j) s_ = s_ - row[j] * x[j];
+    x[i] = shfl_d(s_ / row[i], i);
+  }
+  return 0;
+}
+
+// registration.py:479-494 (see solve_normal_equations)
+__device__ __forceinline__ int warp_solve_normal_equations(const double* h, const double* g, double* xi, int lane) {
+  const double pi2 = CUDART_PI * CUDART_PI;
+  for (int damped = 0; damped < 2; ++damped) {
+    if (warp_solve6(h, damped ? 1e-6 : 0.0, g, xi, lane)) continue;
+    bool fin = true;
+    for (int i = 0; i < 6; ++i) fin = fin && isfinite(xi[i]);
+    if (fin && xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2] < pi2 &&
+        xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5] < 1.0)
+      return 0;
+  }
+  return 1;
+}
+
+// Fused iteration step: linearise (gicp_lin_kernel's body) -> 6x6 solve -> step halving (gicp_halve_kernel's body) by the
+// same warp.  The 80-byte match records {W, index pair} the halving reads are the ones this warp wrote a moment ago:
+// they are still in L2 (cache-global stores / loads) instead of making a round trip through DRAM between two kernels
+// (round 1: 105 GB of the step's 129 GB of DRAM traffic).  Arithmetic and its order are those of the split kernels.
+__global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_kernel(RefineArgs a, int it) {
+  extern __shared__ __align__(16) double sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * PX_GICP_WARPS + wid;
+  if (c >= a.src.n) return;
+  int* st = a.st_i + 8 * (size_t)c;
+  if (st[ST_DONE]) return;
+  double* stage = sm + (size_t)wid * WARP_SM_DOUBLES;  // [43][STAGE_LD]
+  double* hg = stage + 43 * STAGE_LD;                  // [43]: H (36), g (6), f0
+  const CandView v = cand_view(a, c);
+  const int n = v.n;
+  const double* soa = a.src_soa + v.off;  // planes x, y, z, v0x, v0y, v0z
+  const long long plane = a.plane;
+  double* wb = a.w_buf + v.off;           // 10 compact planes
+  const int32_t* nn = a.nn + v.off;
+  const double* tsoa = a.tgt.soa + v.toff;  // same six planes of the target
+  const double f_src = 1.0 - a.cfg.eps, f_tgt = a.tgt.f;
+  const long long tplane = a.tgt.plane;
+  double* pose = a.st_pose + ST_POSE_LD * (size_t)c;
+  double r[9], t[3];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) r[q] = pose[q];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
+
+  double acc0 = 0.0, acc1 = 0.0;
+  // the running match count lives in shared memory: as a register it gets spilled, and the local-memory reload
+  // queues behind the compaction stores (20 % of this kernel's stall samples)
+  volatile int* n_corr_sm = reinterpret_cast<volatile int*>(hg + 43);
+  if (lane == 0) *n_corr_sm = 0;
+  __syncwarp();
+  // software pipeline: a chunk's operands (source point + covariance, gathered target point +
+  // covariance) are requested before the ordered sums of the previous chunk, its neighbour
+  // indices one chunk earlier still
+  int bj_cur = lane < n ? nn[lane] : -1;
+  int bj_next = lane + 32 < n ? nn[lane + 32] : -1;
+  double in[12];  // ax ay az | source v0 | tx ty tz | target v0
+#pragma unroll
+  for (int q = 0; q < 12; ++q) in[q] = 0.0;
+  if (bj_cur >= 0) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) in[q] = PX_LDCS(soa + q * plane + lane);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) in[6 + q] = __ldg(tsoa + q * tplane + bj_cur);
+  }
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const int bj = bj_cur;
+    bool on = false;
+    // absent points keep all-zero inputs: every staged term is then an exact (+-)0, which leaves the
+    // never-negative-zero accumulators unchanged -- and all lanes run one uniform staging pass
+    double w[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double px = 0, py = 0, pz = 0, dx = 0, dy = 0, dz = 0;
+    const double ax = in[0], ay = in[1], az = in[2], tx = in[6], ty = in[7], tz = in[8];
+    if (bj >= 0) {
+      double cai[9], cbj[9];
+      cov_from_normal(in[3], in[4], in[5], f_src, cai);
+      cov_from_normal(in[9], in[10], in[11], f_tgt, cbj);
+      double rc[9], m[9];
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int w_ = 0; w_ < 3; ++w_) {
+          double s_ = 0.0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) s_ += r[3 * u + q] * cai[3 * q + w_];
+          rc[3 * u + w_] = s_;
+        }
+#pragma unroll
+      for (int u = 0; u < 3; ++u)
+#pragma unroll
+        for (int w_ = 0; w_ < 3; ++w_) {
+          double s_ = 0.0;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) s_ += rc[3 * u + q] * r[3 * w_ + q];
+          m[3 * u + w_] = cbj[3 * u + w_] + s_;
+        }
+      const double det = (m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                          m[2] * (m[3] * m[7] - m[4] * m[6]));
+      if (!(det <= 0.0) && isfinite(det)) {
+        on = true;
+        const double inv_det = 1.0 / det;
+        w[0] = (m[4] * m[8] - m[5] * m[7]) * inv_det;
+        w[1] = (m[2] * m[7] - m[1] * m[8]) * inv_det;
+        w[2] = (m[1] * m[5] - m[2] * m[4]) * inv_det;
+        w[3] = (m[5] * m[6] - m[3] * m[8]) * inv_det;
+        w[4] = (m[0] * m[8] - m[2] * m[6]) * inv_det;
+        w[5] = (m[2] * m[3] - m[0] * m[5]) * inv_det;
+        w[6] = (m[3] * m[7] - m[4] * m[6]) * inv_det;
+        w[7] = (m[1] * m[6] - m[0] * m[7]) * inv_det;
+        w[8] = (m[0] * m[4] - m[1] * m[3]) * inv_det;
+        px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
+        py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
+        pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
+        dx = tx - px, dy = ty - py, dz = tz - pz;
+      }
+    }
+    {
+      // J = [ [p]x | -I ] (registration.py:296-309).  The products with J's exact
+      // zeros and -1s are dropped / turned into negations below: x*0 = +-0 and
+      // a + (+-0) = a never change a non-zero value, (-1)*x = -x and a + (-b) = a - b
+      // are exact, and the sign of an all-zero term cannot survive the +0-initialised
+      // accumulators -- so every staged term has the reference's bits.
+      const double wd0 = w[0] * dx + w[1] * dy + w[2] * dz;
+      const double wd1 = w[3] * dx + w[4] * dy + w[5] * dz;
+      const double wd2 = w[6] * dx + w[7] * dy + w[8] * dz;
+      stage[42 * STAGE_LD + lane] = dx * wd0 + dy * wd1 + dz * wd2;
+      // g[u] -= J[0][u]*wd0 + J[1][u]*wd1 + J[2][u]*wd2  (staged negated)
+      stage[36 * STAGE_LD + lane] = -(pz * wd1 - py * wd2);
+      stage[37 * STAGE_LD + lane] = -(px * wd2 - pz * wd0);
+      stage[38 * STAGE_LD + lane] = -(py * wd0 - px * wd1);
+      stage[39 * STAGE_LD + lane] = wd0;
+      stage[40 * STAGE_LD + lane] = wd1;
+      stage[41 * STAGE_LD + lane] = wd2;
+      // wj[q][u] = w[q][0]*J[0][u] + w[q][1]*J[1][u] + w[q][2]*J[2][u]
+      double wj[3][6];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        wj[q][0] = w[3 * q + 1] * pz - w[3 * q + 2] * py;
+        wj[q][1] = w[3 * q + 2] * px - w[3 * q] * pz;
+        wj[q][2] = w[3 * q] * py - w[3 * q + 1] * px;
+        wj[q][3] = -w[3 * q], wj[q][4] = -w[3 * q + 1], wj[q][5] = -w[3 * q + 2];
+      }
+      // h[u][v] += J[0][u]*wj[0][v] + J[1][u]*wj[1][v] + J[2][u]*wj[2][v]
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        stage[(0 + u) * STAGE_LD + lane] = pz * wj[1][u] - py * wj[2][u];
+        stage[(6 + u) * STAGE_LD + lane] = px * wj[2][u] - pz * wj[0][u];
+        stage[(12 + u) * STAGE_LD + lane] = py * wj[0][u] - px * wj[1][u];
+        stage[(18 + u) * STAGE_LD + lane] = -wj[0][u];
+        stage[(24 + u) * STAGE_LD + lane] = -wj[1][u];
+        stage[(30 + u) * STAGE_LD + lane] = -wj[2][u];
+      }
+    }
+    const unsigned onm = __ballot_sync(0xffffffffu, on);
+    if (on) {  // ordered compaction for the halving kernel
+      double* o = wb + *n_corr_sm + __popc(onm & ((1u << lane) - 1u));
+#pragma unroll
+      for (int q = 0; q < 9; ++q) __stcg(o + q * plane, w[q]);  // L2-resident: re-read below by this very warp
+      // tenth plane: (source index, target index) -- the halving kernel fetches the two points itself
+      __stcg(reinterpret_cast<long long*>(o + 9 * plane), (long long)(unsigned)i | ((long long)bj << 32));
+    }
+    __syncwarp();
+    if (lane == 0) *n_corr_sm += __popc(onm);
+    __syncwarp();  // stage writes visible to the summing lanes
+    // next chunk's operands: requested last, so that nothing between here and the end of the ordered
+    // sums has to wait on a long-latency scoreboard they share
+    bj_cur = bj_next;
+    bj_next = i + 64 < n ? nn[i + 64] : -1;
+    if (bj_cur >= 0) {
+#pragma unroll
+      for (int q = 0; q < 6; ++q) in[q] = PX_LDCS(soa + q * plane + i + 32);  // streamed once per iteration
+#pragma unroll
+      for (int q = 0; q < 6; ++q) in[6 + q] = __ldg(tsoa + q * tplane + bj_cur);
+    }
+    {
+      const double* row0 = stage + lane * STAGE_LD;
+      const double* row1 = stage + (lane + 32) * STAGE_LD;
+      const bool second = lane < 11;  // quantities 32..42
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        acc0 += row0[j];
+        if (second) acc1 += row1[j];  // predicated, not a branch
+      }
+    }
+    __syncwarp();
+  }
+  // ---- the sums are complete: H (36), g (6), f0 into this warp's shared memory ----
+  hg[lane] = acc0;
+  if (lane < 11) hg[32 + lane] = acc1;
+  __syncwarp();
+  const int nc = *n_corr_sm;
+  if (lane == 0) {
+    st[ST_ITERS] = it;
+    st[ST_NCORR] += nc;
+    st[ST_NCOMPACT] = nc;
+  }
+  // ---- registration.py:434-437 + :479-494: degenerate / singular exits, else the step xi (rows of the augmented
+  // system in lanes 0..5: the same partial-pivot LU as solve6, operation for operation) ----
+  double xi[6] = {0, 0, 0, 0, 0, 0};
+  int failure0 = F_OK;
+  if (nc < 6)
+    failure0 = F_DEGENERATE;
+  else if (warp_solve_normal_equations(hg, hg + 36, xi, lane))
+    failure0 = F_SINGULAR;
+  if (failure0 != F_OK) {
+    if (lane == 0) st[ST_FAIL] = failure0, st[ST_DONE] = 1;
+    return;
+  }
+  const double f0 = hg[42];
+  const GicpCfgDev cfg = a.cfg;
+  // ---- step halving over the match records this warp has just written (L2 hits) ----
+  constexpr int NTMAX = PX_HALVE_NTMAX;
+  __syncwarp();  // hg has been read by every lane; the staging rows are free
+  double(*sm_pose)[12] = reinterpret_cast<double(*)[12]>(stage);              // [NTMAX][12]
+  double(*sm_term)[32] = reinterpret_cast<double(*)[32]>(stage + NTMAX * 12);  // [NTMAX][32]
+  int acc_s = -1, acc_tr = 0;
+  double f_acc = 0.0;
+  int NT = st[ST_LASTTR] >= PX_HALVE_NT ? NTMAX : PX_HALVE_NT;  // trials in the first pass (a power of two)
+  for (int tr0 = 0; tr0 < 9 && acc_s < 0; tr0 += NT, NT = PX_HALVE_NT) {
+    const int my = lane & (NT - 1);  // the trial of the pass whose pose this lane builds and whose sum it carries
+    {
+      double r[9], t[3], rs[9];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) r[q] = pose[q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) t[q] = pose[9 + q];
+      const double scale = 1.0 / (double)(1 << (tr0 + my));  // exact power of two, as `scale *= 0.5` yields
+      so3_exp_fast(scale * xi[0], scale * xi[1], scale * xi[2], rs);
+      __syncwarp();
+      if (lane < NT) {
+        double* o = sm_pose[lane];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            o[3 * i + j] = dot_f012(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], r[j], r[3 + j], r[6 + j]);
+          o[9 + i] = dot_f102(rs[3 * i], rs[3 * i + 1], rs[3 * i + 2], t[0], t[1], t[2]) + scale * xi[3 + i];
+        }
+      }
+      __syncwarp();
+    }
+    // ---- fixed-association objective (registration.py:387-407) of the NT trial poses ----
+    double f = 0.0;
+    double cur[15];  // W (9) | source point (3) | target point (3)
+    // software pipeline: the (source, target) index pair of a chunk is fetched one chunk ahead of its operands
+    long long ij_cur = lane < nc ? __ldcg(reinterpret_cast<const long long*>(wb + 9 * plane) + lane) : 0;
+    long long ij_next = lane + 32 < nc ? __ldcg(reinterpret_cast<const long long*>(wb + 9 * plane) + lane + 32) : 0;
+    if (lane < nc) {
+      const int si = (int)(unsigned)ij_cur, tj = (int)(ij_cur >> 32);
+#pragma unroll
+      for (int q = 0; q < 9; ++q) cur[q] = __ldcg(wb + q * plane + lane);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
+    }
+    for (int base = 0; base < nc; base += 32) {
+      const int k = base + lane;
+      const bool have = k < nc;
+#pragma unroll
+      for (int s_ = 0; s_ < NTMAX; ++s_) {
+        if (s_ >= NT) break;
+        double term = 0.0;
+        if (have) {
+          const double* P = sm_pose[s_];
+          const double px = P[0] * cur[9] + P[1] * cur[10] + P[2] * cur[11] + P[9];
+          const double py = P[3] * cur[9] + P[4] * cur[10] + P[5] * cur[11] + P[10];
+          const double pz = P[6] * cur[9] + P[7] * cur[10] + P[8] * cur[11] + P[11];
+          const double dx = cur[12] - px, dy = cur[13] - py, dz = cur[14] - pz;
+          const double wd0 = cur[0] * dx + cur[1] * dy + cur[2] * dz;
+          const double wd1 = cur[3] * dx + cur[4] * dy + cur[5] * dz;
+          const double wd2 = cur[6] * dx + cur[7] * dy + cur[8] * dz;
+          term = dx * wd0 + dy * wd1 + dz * wd2;
+        }
+        sm_term[s_][lane] = term;
+      }
+      __syncwarp();
+      ij_cur = ij_next;
+      ij_next = k + 64 < nc ? __ldcg(reinterpret_cast<const long long*>(wb + 9 * plane) + k + 64) : 0;
+      if (k + 32 < nc) {  // next chunk's operands are in flight during the ordered sums
+        const int si = (int)(unsigned)ij_cur, tj = (int)(ij_cur >> 32);
+#pragma unroll
+        for (int q = 0; q < 9; ++q) cur[q] = __ldcg(wb + q * plane + k + 32);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
+      }
+      const double2* s2 = reinterpret_cast<const double2*>(sm_term[my]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double2 v = s2[j];
+        f += v.x;
+        f += v.y;
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int s_ = NTMAX - 1; s_ >= 0; --s_) {  // first acceptable trial in trial order
+      const double fs = shfl_d(f, s_);
+      if (s_ < NT && tr0 + s_ < 9 && isfinite(fs) && fs <= f0) acc_s = s_, acc_tr = tr0 + s_, f_acc = fs;
+    }
+  }
+  int failure = F_OK, conv = 0;
+  bool done = false;
+  if (acc_s < 0) {
+    failure = F_NO_DECREASE, done = true;
+  } else {
+    const double* P = sm_pose[acc_s];
+    double r_try[9], r[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) r_try[q] = P[q];
+    renorm_rotation(r_try, r);
+    const double scale = 1.0 / (double)(1 << acc_tr), f_try = f_acc;
+    if (a.out_trace && lane == 0) {
+      double* trace = a.out_trace + 2 * (size_t)cfg.max_iter * c;
+      trace[2 * (it - 1)] = f0, trace[2 * (it - 1) + 1] = f_try;
+    }
+    const double step_t2 = scale * scale * (xi[3] * xi[3] + xi[4] * xi[4] + xi[5] * xi[5]);
+    const double step_r2 = scale * scale * (xi[0] * xi[0] + xi[1] * xi[1] + xi[2] * xi[2]);
+    if (step_t2 < cfg.tol_t2 && step_r2 < cfg.tol_r2)
+      conv = 1, done = true;
+    else if (it >= 5 && f0 > 0.0 && (f0 - f_try) <= 1e-4 * f0)
+      done = true;
+    if (lane < 9) pose[lane] = r[lane];
+    if (lane < 3) pose[9 + lane] = P[9 + lane];
+  }
+  if (lane == 0) {
+    if (failure != F_OK) st[ST_FAIL] = failure;
+    if (failure == F_OK) st[ST_NTRACE] = it, st[ST_LASTTR] = acc_tr;  // an accepted step was recorded
+    if (conv) st[ST_CONV] = 1;
+    if (done || it >= cfg.max_iter) st[ST_DONE] = 1;
+  }
+}
+
 __global__ void __launch_bounds__(128) gicp_finish_kernel(RefineArgs a) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + wid;
@@ -1303,6 +1680,7 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   gicp_init_kernel<<<(unsigned)(((long long)a.src.n * init_split + 3) / 4), 128, smem_init, st>>>(a, init_split);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(gicp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   cudaFuncSetAttribute(gicp_nn_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);  // all of it as L1
   const int blocks = (a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS;
   // enough NN warps for ~one full wave (148 SMs x 32 warps) when the batch is small
@@ -1314,16 +1692,25 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
     PX_MARK();
     gicp_nn_kernel<<<(unsigned)(((long long)a.src.n * nn_split + 3) / 4), 128, 0, st>>>(a, it, nn_split);
     PX_MARK();
+#ifdef PX_GICP_SPLIT
     gicp_lin_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
     gicp_solve_kernel<<<(a.src.n + 127) / 128, 128, 0, st>>>(a);  // timed together with the linearisation
     PX_MARK();
     gicp_halve_kernel<<<b4, 128, 0, st>>>(a, it);
+#else
+    gicp_step_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);  // linearise + solve + halving, one warp per candidate
+    PX_MARK();
+#endif
   }
   PX_MARK();
   gicp_finish_kernel<<<b4, 128, 0, st>>>(a);
   PX_MARK();
 #undef PX_MARK
+#ifdef PX_GICP_SPLIT
   if (launches) *launches = 2 + 4 * std::max(a.cfg.max_iter, 0);
+#else
+  if (launches) *launches = 2 + 2 * std::max(a.cfg.max_iter, 0);
+#endif
 #ifdef PX_NN_STATS
   cudaStreamSynchronize(st);
   dump_nn_stats();

@@ -555,7 +555,9 @@ class Engine:
         N.check(self.ctx, rc, "px_search_stats")
         return nc, c0, c1, nm, nfp
 
-    KERNELS = ("gicp_init_kernel", "gicp_nn_kernel", "gicp_lin_kernel", "gicp_halve_kernel", "gicp_finish_kernel")
+    # gicp_step_kernel = linearise + solve + step halving fused (the default build); a -DPX_GICP_SPLIT build runs
+    # gicp_lin_kernel (+ solve) and gicp_halve_kernel instead and reports them in the third / fourth slot
+    KERNELS = ("gicp_init_kernel", "gicp_nn_kernel", "gicp_step_kernel", "gicp_halve_kernel", "gicp_finish_kernel")
 
     def set_kernel_timing(self, on: bool):
         N.check(self.ctx, self.lib.px_ctx_set_kernel_timing(self.ctx, int(on)), "px_ctx_set_kernel_timing")

@@ -6,7 +6,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 tag = sys.argv[1]
 wl = sys.argv[2] if len(sys.argv) > 2 else "c3"
-names = {"gicp_nn": "gicp_nn_kernel", "gicp_lin": "gicp_lin_kernel", "gicp_halve": "gicp_halve_kernel",
+names = {"gicp_nn": "gicp_nn_kernel", "gicp_step": "gicp_step_kernel", "gicp_lin": "gicp_lin_kernel", "gicp_halve": "gicp_halve_kernel",
          "gicp_init": "gicp_init_kernel", "render_kernel": "render_kernel", "cost_kernel": "cost_kernel"}
 tj = ROOT / "profiles" / "traffic.json"
 db = json.loads(tj.read_text()) if tj.exists() else {}
@@ -31,7 +31,7 @@ for short, full in names.items():
         "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
         "duration_ms_under_ncu": val("gpu__time_duration.sum"),
         "source": f"profiles/{summ.name} (ncu --set full --clock-control none, " +
-                  ("launch #9 of 30, " if short in ("gicp_nn", "gicp_lin", "gicp_halve") else "") + f"{wl.upper()} 58,320 candidates)",
+                  ("launch #9 of 30, " if short in ("gicp_nn", "gicp_step", "gicp_lin", "gicp_halve") else "") + f"{wl.upper()} 58,320 candidates)",
         "ncu": {"issue_slots_busy_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active", False),
                 "fp64_pipe_pct": val("sm__inst_executed_pipe_fp64.sum.pct_of_peak_sustained_active", False),
                 "dram_pct_of_peak": val("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", False),
