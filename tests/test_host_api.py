@@ -234,3 +234,35 @@ def test_bench_gpus_flag_spawns_one_rank_per_gpu(monkeypatch):
     cmd = json.loads(out.strip().splitlines()[-1])
     assert "torch.distributed.run" in cmd and "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
     assert cmd[-4:] == ["--gpus", "4", "--steps", "2"]
+
+
+@pytest.mark.parametrize("name,over", [("c1_box_3dof", {}), ("c2_twocyl_color1", {}),
+                                       ("c4_mixed_6dof", dict(viewpoints=8, n_inplane=3, max_proposals=None))])
+def test_lattice_plan_factors_reproduce_the_flat_plan(name, over):
+    """plan_lattice hands the device each object's proposal set as outer x inner FACTORS (px_search_upload_lattice);
+    expanding them on the host with the reference's own composition gives exactly plan_search's flat candidate
+    list (object ids, poses, counts, provenance) -- the GPU test checks the device expansion against the same arrays."""
+    import dataclasses
+    from paper_2008_00326_b200.geometry import RigidTransform
+    from paper_2008_00326_b200.search import plan_lattice
+    d, frame, models, cfg, _ = G.scene(name)
+    cfg = dataclasses.replace(cfg, **over)
+    flat = plan_search(frame, models, cfg, build_targets=False)
+    lat = plan_lattice(frame, models, cfg)
+    assert lat.n == flat.n and lat.active == flat.active and lat.object_ids == flat.object_ids
+    w2c = RigidTransform.from_matrix3x4(flat.w2c) if flat.w2c_vec_order == 0 else flat.cam_to_world.inverse()
+    row = 0
+    for f in lat.lattice:
+        assert lat.count_of(f.object_id) == flat.count_of(f.object_id) == f.n_outer * f.n_inner
+        for outer in range(f.n_outer):
+            for inner in range(0, f.n_inner, max(1, f.n_inner // 3)):
+                j = row + outer * f.n_inner + inner
+                if cfg.mode == "3dof":
+                    pose = w2c.compose(RigidTransform(f.rotations[inner].copy(), f.translations[outer].copy()))
+                    want = np.concatenate([pose.rotation, pose.translation[:, None]], axis=1)
+                else:
+                    want = np.concatenate([f.rotations[outer], f.translations[inner][:, None]], axis=1)
+                assert np.array_equal(flat.cam_poses[j], want)
+                assert lat.provenance_of(f.object_id, outer * f.n_inner + inner) == flat.provenance_of(f.object_id, outer * f.n_inner + inner)
+        row += f.n_outer * f.n_inner
+    assert plan_lattice(frame, models, dataclasses.replace(cfg, max_proposals=10)) is None  # subsampling needs the flat plan
