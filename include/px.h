@@ -251,7 +251,8 @@ int px_comm_info(const px_ctx* ctx, int32_t* rank, int32_t* world, int32_t* nccl
  * the communicator (skipped when px_comm_init was not called), then the record of every model's
  * winning candidate is extracted on the device and, across ranks, delivered to every rank by an
  * all-reduce(MAX) over the records' raw 64-bit words (only the owning rank's record is non-zero).
- * The keys px_search_download returns afterwards are the global ones. */
+ * The keys px_search_download returns afterwards are the global ones.  Every rank must have uploaded the same
+ * models in the same order (records are indexed by model slot). */
 int px_search_reduce(px_ctx* ctx);
 /* Per uploaded model, in upload order (any pointer may be NULL): global packed key (UINT64_MAX = no
  * candidate), the winner's refined candidate pose (12) and applied GICP correction (12), its j_o, j_r,

@@ -85,12 +85,22 @@ def m2m_gicp(sources, targets, inits, cfg: GicpConfig, target_indices=None,
 
 def gicp_align(source, target, source_covs, target_covs, init: RigidTransform,
                cfg: GicpConfig) -> RegistrationResult:
-    """Single-pair GICP (registration.py:410-476).  The covariances are rebuilt
-    on the device from the clouds with cfg's (k, epsilon); passing covariances
-    computed with other parameters is not supported."""
+    """Single-pair GICP (registration.py:410-476).  The device rebuilds the covariances from the clouds
+    with cfg's (k, epsilon) -- exactly what every caller on the search path passes (registration.py:500-511).
+    Covariances that are NOT `estimate_covariances(cloud, cfg.k_covariance, cfg.epsilon)` would silently be
+    ignored, so they are refused instead (DeviceError): a limit reported, never a different answer."""
+    from .errors import DeviceError
+
     src, tgt = _pts(source), _pts(target)
     if src.shape[0] < 3 or tgt.shape[0] < 3:
         return RegistrationResult(init, 0, float("inf"), False, "degenerate_correspondences")
+    for pts, covs, what in ((src, source_covs, "source"), (tgt, target_covs, "target")):
+        if covs is None or pts.shape[0] <= cfg.k_covariance:
+            continue
+        given = np.asarray(covs, dtype=np.float64).reshape(-1, 3, 3)
+        if given.shape[0] != pts.shape[0] or not np.array_equal(given, estimate_covariances(pts, cfg.k_covariance, cfg.epsilon)):
+            raise DeviceError(f"gicp_align: the {what} covariances differ from estimate_covariances(cloud, "
+                              f"{cfg.k_covariance}, {cfg.epsilon}); the device path builds its own and cannot honour others")
     return m2m_gicp([src], [tgt], [init], cfg, [0])[0]
 
 

@@ -311,3 +311,16 @@ def test_cli_estimate_many(engine, tmp_path):
     for p in dirs:
         assert (p / "results.json").read_text() == want
         assert set(json.loads((p / "timings.json").read_text())) == {"total_millis", "stage_millis", "per_object_millis"}
+
+
+def test_gicp_align_refuses_foreign_covariances(engine):
+    """registration.gicp_align(source, target, source_covs, target_covs, ...): the device builds its own covariances;
+    the reference's own ones are accepted (bit-equal), anything else is an error instead of being silently ignored."""
+    from paper_2008_00326_b200 import RigidTransform, registration
+    src, tgt, ca, cb = (U[f"gicp0_{k}"] for k in ("src", "tgt", "ca", "cb"))
+    cfg = GicpConfig()
+    res = registration.gicp_align(src, tgt, ca, cb, RigidTransform.identity(), cfg)
+    assert res.iterations == int(U["gicp0_iters"]) and res.failure is None
+    with pytest.raises(DeviceError, match="covariances differ"):
+        registration.gicp_align(src, tgt, ca * 1.5, cb, RigidTransform.identity(), cfg)
+    assert registration.gicp_align(src, tgt, None, None, RigidTransform.identity(), cfg).iterations == res.iterations
