@@ -1046,6 +1046,7 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     a.points = ctx->tgt_pts.as<double>(), a.cov = ctx->tgt_cov.as<double>(), a.v0 = ctx->tgt_v0.as<double>(), a.k = k, a.eps = cfg->epsilon;
     if (org) a.org = ctx->tgt_org.as<TgtOrg>(), a.tmap = ctx->tgt_map.as<int32_t>(), a.tpix = ctx->tgt_pix.as<int32_t>();
     a.ray_k = ctx->cam.ray_k;
+    if (org) a.cam = ctx->cam;
     CU(launch_cov(a, total, ctx->stream));
     CU(ctx->tgt_soa.ensure(tot1 * 72));
     CU(launch_soa(ctx->tgt_pts.as<double>(), ctx->tgt_v0.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
@@ -1072,6 +1073,7 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   a.obs_cell = ctx->obs_cell.as<int32_t>(), a.gidx = ctx->gidx.as<int32_t>(), a.n_obs = ctx->n_obs, a.GW = ctx->cam.GW;
   a.world = ctx->tgt_world.as<double>();
   a.gate = cfg->max_correspondence_distance;
+  a.cam = ctx->cam;
   {
     // frame of the fp32 pruning structures: in 3-DoF the world frame, where the supporting plane (most of every
     // capsule crop) is axis-aligned; re-orthonormalised here (Gram-Schmidt in fp64) because the error bound of the
@@ -1137,7 +1139,7 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
     CovArgs c{};
     c.n_clouds = n, c.offset = off, c.count = nullptr;
     c.points = a.tgt_pts, c.cov = ctx->tgt_cov.as<double>(), c.v0 = ctx->tgt_v0.as<double>(), c.k = k, c.eps = cfg->epsilon;
-    c.org = a.org, c.tmap = a.tmap, c.tpix = a.tpix, c.ray_k = ctx->cam.ray_k;
+    c.org = a.org, c.tmap = a.tmap, c.tpix = a.tpix, c.ray_k = ctx->cam.ray_k, c.cam = ctx->cam;
     CU(launch_cov(c, total, ctx->stream));
     CU(launch_soa(a.tgt_pts, ctx->tgt_v0.as<double>(), ctx->tgt_soa.as<double>(), total, ctx->stream));
     ctx->launches += 5;

@@ -329,10 +329,11 @@ __global__ void __launch_bounds__(128) cov_kernel(CovArgs a) {
   if (org) {
     const TgtOrg o = a.org[c];
     OrgView V{a.points + 3 * off, a.tmap + o.map_off, o.w, o.h};
+    const double ray_k = a.cam.stride > 0 ? window_ray_k(a.cam, o.gx0, o.gy0, o.w, o.h) : a.ray_k;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int cell = a.tpix[off + i];
       double cv[12];
-      cov_point_org(V, i, cell % o.w, cell / o.w, a.k, a.eps, a.ray_k, cv);
+      cov_point_org(V, i, cell % o.w, cell / o.w, a.k, a.eps, ray_k, cv);
       store_cov(a, off + i, cv);
     }
   } else {

@@ -129,6 +129,7 @@ struct TgtBuildArgs {
   double c2w[12];             // camera -> world (mode 0)
   double gate;                // max_correspondence_distance (enters the fp32 pruning error bound)
   double frame[9];            // TargetsDev::rot: frame of the fp32 pruning structures
+  Camera cam;                 // intrinsics + grid size (mode 0: screen window of a capsule)
   // scene
   const double* obs_pts;      // (n_obs,3) camera frame
   const int32_t* obs_labels;  // (n_obs)
@@ -172,6 +173,7 @@ struct CovArgs {  // covariances of a list of clouds (targets), thread per point
   const int32_t* tmap;
   const int32_t* tpix;      // (sum) map cell (y*w+x) of every target point
   double ray_k;
+  Camera cam;               // ray_k is re-derived per target over its own grid window when cam.stride > 0
 };
 cudaError_t launch_cov(const CovArgs& a, long long total_points, cudaStream_t st);
 // (n,3) points + (n,3) covariance normals -> 6 planes of n doubles (TargetsDev::soa)

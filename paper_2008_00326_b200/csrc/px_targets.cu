@@ -32,6 +32,33 @@ __device__ __forceinline__ bool tgt_member(const TgtBuildArgs& a, int t, long lo
   return dx * dx + dy * dy + dz * dz <= prm[4] * prm[4];
 }
 
+// Stride-grid window that contains the projection of every point a capsule can hold: the capsule
+// {dx^2 + dy^2 + max(z_lo - z, z - z_hi, 0)^2 <= radius^2} lies inside the ball of radius R = radius + (z_hi - z_lo) / 2
+// around its mid point; with the ball in front of the camera (z_c - R > 0) the extreme image coordinates of the ball's
+// bounding cube bound the projections.  Two cells of margin on every side; the whole grid when no bound exists.
+__device__ __forceinline__ void capsule_window(const TgtBuildArgs& a, const double* prm, int& gx_lo, int& gx_hi, int& gy_lo,
+                                               int& gy_hi) {
+  const int GW = a.cam.GW, GH = a.cam.GH;
+  gx_lo = 0, gy_lo = 0, gx_hi = GW - 1, gy_hi = GH - 1;
+  const double R = prm[4] + 0.5 * fabs(prm[3] - prm[2]);
+  // capsule mid point in the camera frame: R_c2w^T (c - t_c2w)
+  const double wx = prm[0] - a.c2w[3], wy = prm[1] - a.c2w[7], wz = 0.5 * (prm[2] + prm[3]) - a.c2w[11];
+  const double xc = a.c2w[0] * wx + a.c2w[4] * wy + a.c2w[8] * wz;
+  const double yc = a.c2w[1] * wx + a.c2w[5] * wy + a.c2w[9] * wz;
+  const double zc = a.c2w[2] * wx + a.c2w[6] * wy + a.c2w[10] * wz;
+  const double zn = zc - R * 1.001 - 1e-6, zf = zc + R * 1.001 + 1e-6;
+  if (!(zn > 1e-3) || !isfinite(xc + yc + zc + R)) return;
+  const double x0 = xc - R * 1.001, x1 = xc + R * 1.001, y0 = yc - R * 1.001, y1 = yc + R * 1.001;
+  const double ulo = a.cam.cx + a.cam.fx * fmin(x0 / zn, x0 / zf), uhi = a.cam.cx + a.cam.fx * fmax(x1 / zn, x1 / zf);
+  const double vlo = a.cam.cy + a.cam.fy * fmin(y0 / zn, y0 / zf), vhi = a.cam.cy + a.cam.fy * fmax(y1 / zn, y1 / zf);
+  const double st = (double)a.cam.stride;
+  // observed point of grid cell g sits at pixel g * stride + 0.5
+  const double a0 = floor((ulo - 0.5) / st) - 2.0, a1 = ceil((uhi - 0.5) / st) + 2.0;
+  const double b0 = floor((vlo - 0.5) / st) - 2.0, b1 = ceil((vhi - 0.5) / st) + 2.0;
+  gx_lo = (int)fmin(fmax(a0, 0.0), (double)GW), gx_hi = (int)fmax(fmin(a1, (double)(GW - 1)), -1.0);
+  gy_lo = (int)fmin(fmax(b0, 0.0), (double)GH), gy_hi = (int)fmax(fmin(b1, (double)(GH - 1)), -1.0);
+}
+
 // pass 1: member count and grid bounding box of every target
 __global__ void __launch_bounds__(256) tgt_count_kernel(TgtBuildArgs a) {
   const int t = blockIdx.x;
@@ -40,11 +67,24 @@ __global__ void __launch_bounds__(256) tgt_count_kernel(TgtBuildArgs a) {
   if (a.mode == 0 && threadIdx.x < 5) prm[threadIdx.x] = a.params[5 * (size_t)t + threadIdx.x];
   __syncthreads();
   int cnt = 0, x0 = 1 << 30, y0 = 1 << 30, x1 = -1, y1 = -1;
-  for (long long i = threadIdx.x; i < a.n_obs; i += blockDim.x)
-    if (tgt_member(a, t, i, prm)) {
-      const int cell = a.obs_cell[i], gx = cell % a.GW, gy = cell / a.GW;
-      ++cnt, x0 = min(x0, gx), x1 = max(x1, gx), y0 = min(y0, gy), y1 = max(y1, gy);
+  if (a.mode == 0) {
+    // only the cells inside the capsule's screen window can hold members (the predicate itself is unchanged)
+    int gx_lo, gx_hi, gy_lo, gy_hi;
+    capsule_window(a, prm, gx_lo, gx_hi, gy_lo, gy_hi);
+    const int ww = gx_hi - gx_lo + 1, wh = gy_hi - gy_lo + 1;
+    const int ncell = (ww > 0 && wh > 0) ? ww * wh : 0;
+    for (int q = threadIdx.x; q < ncell; q += blockDim.x) {
+      const int gx = gx_lo + q % ww, gy = gy_lo + q / ww;
+      const long long i = a.gidx[gy * a.GW + gx];
+      if (i >= 0 && tgt_member(a, t, i, prm)) ++cnt, x0 = min(x0, gx), x1 = max(x1, gx), y0 = min(y0, gy), y1 = max(y1, gy);
     }
+  } else {
+    for (long long i = threadIdx.x; i < a.n_obs; i += blockDim.x)
+      if (tgt_member(a, t, i, prm)) {
+        const int cell = a.obs_cell[i], gx = cell % a.GW, gy = cell / a.GW;
+        ++cnt, x0 = min(x0, gx), x1 = max(x1, gx), y0 = min(y0, gy), y1 = max(y1, gy);
+      }
+  }
   for (int o = 16; o; o >>= 1) {
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o)), y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
