@@ -285,7 +285,7 @@ def run_gpu(args):
     model_bytes = sum(m.mesh.vertices.size * 16 + m.mesh.triangles.size * 4 for m in models.values())
     if lat is not None:
         ng = ((k_.width + cfg.stride - 1) // cfg.stride) * ((k_.height + cfg.stride - 1) // cfg.stride)
-        h2d = npix * 13 + ng * 24 + model_bytes + sum(f.rotations.size * 8 + f.translations.size * 8 + 64 for f in lat.lattice)
+        h2d = ng * (13 + 24) + model_bytes + sum(f.rotations.size * 8 + f.translations.size * 8 + 64 for f in lat.lattice)
     else:
         h2d = npix * 13 + len(plan.observed) * (24 + 24 + 8 + 4) + n_specs * 40 + model_bytes + n_local * (96 + 12)
     d2h = 8 * 28 * len(models) + 32

@@ -93,12 +93,15 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
                     const double* obs_points, const double* obs_lab, const int32_t* obs_src_px,
                     const int32_t* obs_labels, int64_t n_obs);
 /* Same, with the observed cloud built ON THE DEVICE from the frame (replaces raster.frame_to_cloud /
- * _grid_cloud / cloud_labels, raster.py:191-217): stride-grid sampling of `valid`, row-major order,
- * unprojection at the pixel centre, sRGB -> Lab, label per point.  color_grid is the (GH,GW,3) float64
- * sRGB image of the stride-grid pixels (frame.color[::stride, ::stride]).  Points, source pixels and labels
- * are bit-identical to the host path; Lab agrees to ~1e-12.  n_obs_out (nullable) receives the cloud size. */
-int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
-                          const int32_t* labels, const double* color_grid, const double intr[4], int32_t stride,
+ * _grid_cloud / cloud_labels, raster.py:191-217): row-major order over the valid stride-grid pixels,
+ * unprojection at the pixel centre, sRGB -> Lab, label per point.  The batch path only ever reads the frame at
+ * the stride-grid pixels (raster.py:263-278), so the four planes are passed already sampled there --
+ * plane[::stride, ::stride], C-contiguous, GH = ceil(H/stride) rows of GW = ceil(W/stride): depth (GH,GW) float64,
+ * valid (GH,GW) uint8, labels (GH,GW) int32, colour (GH,GW,3) float64 sRGB; H, W are the full image size.
+ * Points, source pixels and labels are bit-identical to the host path; Lab agrees to ~1e-12.
+ * n_obs_out (nullable) receives the cloud size. */
+int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth_grid, const uint8_t* valid_grid,
+                          const int32_t* labels_grid, const double* color_grid, const double intr[4], int32_t stride,
                           int64_t* n_obs_out);
 /* The resident observed cloud (any pointer may be NULL): points (n,3), Lab (n,3), source pixels (n,2), labels (n). */
 int px_scene_download_cloud(px_ctx* ctx, double* points, double* lab, int32_t* src_px, int32_t* labels);

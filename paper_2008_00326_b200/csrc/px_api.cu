@@ -480,10 +480,22 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   if (int r = set_camera(ctx, H, W, intr, stride)) return r;
   Camera& c = ctx->cam;
   ctx->obs_host_stale = false;
-  const size_t npix = (size_t)H * W;
-  if (int r = h2d(ctx, ctx->depth, depth, npix * sizeof(double))) return r;
-  if (int r = h2d(ctx, ctx->valid, valid, npix)) return r;
-  if (int r = h2d(ctx, ctx->labels, labels, npix * sizeof(int32_t))) return r;
+  {
+    // the batch path only ever reads the frame planes at the stride-grid pixels (raster.py:263-278): keep those
+    const size_t ngrid = (size_t)c.GW * c.GH;
+    std::vector<double> dg(ngrid);
+    std::vector<uint8_t> vg(ngrid);
+    std::vector<int32_t> lg(ngrid);
+    for (int gv = 0; gv < c.GH; ++gv)
+      for (int gu = 0; gu < c.GW; ++gu) {
+        const size_t o = (size_t)gv * stride * W + (size_t)gu * stride, g = (size_t)gv * c.GW + gu;
+        dg[g] = depth[o], vg[g] = valid[o], lg[g] = labels[o];
+      }
+    if (int r = h2d(ctx, ctx->depth, dg.data(), ngrid * sizeof(double))) return r;
+    if (int r = h2d(ctx, ctx->valid, vg.data(), ngrid)) return r;
+    if (int r = h2d(ctx, ctx->labels, lg.data(), ngrid * sizeof(int32_t))) return r;
+    CU(cudaStreamSynchronize(ctx->stream));  // dg / vg / lg are stack-owned
+  }
   if (int r = h2d(ctx, ctx->obs_pts, obs_points, (size_t)n_obs * 24)) return r;
   if (int r = h2d(ctx, ctx->obs_lab, obs_lab, (size_t)n_obs * 24)) return r;
   if (int r = h2d(ctx, ctx->obs_labels, obs_labels, (size_t)n_obs * 4)) return r;
@@ -531,19 +543,19 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
   return 0;
 }
 
-int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
-                          const int32_t* labels, const double* color_grid, const double intr[4], int32_t stride,
+int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth_grid, const uint8_t* valid_grid,
+                          const int32_t* labels_grid, const double* color_grid, const double intr[4], int32_t stride,
                           int64_t* n_obs_out) {
   if (!ctx) return PX_E_ARG;
-  if (H <= 0 || W <= 0 || stride < 1 || !depth || !valid || !labels || !color_grid || !intr)
+  if (H <= 0 || W <= 0 || stride < 1 || !depth_grid || !valid_grid || !labels_grid || !color_grid || !intr)
     return fail(ctx, PX_E_ARG, "px_scene_upload_frame: bad arguments");
   CU(cudaSetDevice(ctx->device));
   if (int r = set_camera(ctx, H, W, intr, stride)) return r;
   const Camera& c = ctx->cam;
-  const size_t npix = (size_t)H * W, ng = (size_t)c.GW * c.GH;
-  if (int r = h2d(ctx, ctx->depth, depth, npix * sizeof(double))) return r;
-  if (int r = h2d(ctx, ctx->valid, valid, npix)) return r;
-  if (int r = h2d(ctx, ctx->labels, labels, npix * sizeof(int32_t))) return r;
+  const size_t ng = (size_t)c.GW * c.GH;
+  if (int r = h2d(ctx, ctx->depth, depth_grid, ng * sizeof(double))) return r;
+  if (int r = h2d(ctx, ctx->valid, valid_grid, ng)) return r;
+  if (int r = h2d(ctx, ctx->labels, labels_grid, ng * sizeof(int32_t))) return r;
   if (int r = h2d(ctx, ctx->color_grid, color_grid, ng * 24)) return r;
   CU(ctx->row_cnt.ensure((size_t)c.GH * 8));
   CU(ctx->row_off.ensure((size_t)c.GH * 8));

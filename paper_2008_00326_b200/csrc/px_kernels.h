@@ -41,7 +41,7 @@ struct RenderArgs {
   int skip_lab;               // 1: leave `lab` unwritten (first render of a refining search: GICP reads points only);
                               // 2: store the linear-light colour there instead (the cost kernel converts on demand)
   double delta_occ;
-  const double* obs_depth;    // (H,W)
+  const double* obs_depth;    // (GH,GW): the observed planes at the stride-grid pixels (all the batch path ever reads)
   const uint8_t* obs_valid;
   const int32_t* obs_labels;
   int4* bbox;                 // (n) out of K0 / in of K1
@@ -269,9 +269,9 @@ cudaError_t launch_winners(const WinnerArgs& a, cudaStream_t st);
 struct SceneCloudArgs {
   int H, W, stride, GW, GH;
   double fx, fy, cx, cy;
-  const double* depth;        // (H,W)
-  const uint8_t* valid;       // (H,W)
-  const int32_t* labels;      // (H,W)
+  const double* depth;        // (GH,GW) stride-grid samples of the frame planes
+  const uint8_t* valid;       // (GH,GW)
+  const int32_t* labels;      // (GH,GW)
   const double* color_grid;   // (GH,GW,3) sRGB of the stride-grid pixels
   long long* row_count;       // (GH) out of the count pass
   const long long* row_offset;  // (GH) exclusive scan

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(PX_RENDER_THREADS) render_kernel(RenderArgs a)
           have = eval_pixel(s, px, py, depth, b0, b1, b2);  // same bits as pass 1
         }
         if (have && !DENSE && a.occluder_marking) {  // raster.py:263-270
-          const size_t o = (size_t)py * cam.W + px;
+          const size_t o = (size_t)(bb.y + r0 + gy) * cam.GW + (bb.x + gx);  // the observed planes are stride-grid sampled
           if (a.obs_valid[o] && a.obs_depth[o] < depth - a.delta_occ && a.obs_labels[o] != m.object_id) have = false;
         }
       }

@@ -20,9 +20,9 @@ namespace px {
 __global__ void __launch_bounds__(128) scene_count_kernel(SceneCloudArgs a) {
   const int gv = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (gv >= a.GH) return;
-  const uint8_t* row = a.valid + (size_t)gv * a.stride * a.W;
+  const uint8_t* row = a.valid + (size_t)gv * a.GW;
   int cnt = 0;
-  for (int gu = lane; gu < a.GW; gu += 32) cnt += row[(size_t)gu * a.stride] != 0;
+  for (int gu = lane; gu < a.GW; gu += 32) cnt += row[gu] != 0;
   for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   if (lane == 0) a.row_count[gv] = cnt;
 }
@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(128) scene_fill_kernel(SceneCloudArgs a) {
     const int gu = g0 + lane;
     const int u = gu * a.stride;
     const bool in = gu < a.GW;
-    const bool ok = in && a.valid[(size_t)v * a.W + u] != 0;
+    const bool ok = in && a.valid[(size_t)gv * a.GW + gu] != 0;
     const unsigned m = __ballot_sync(0xffffffffu, ok);
     const long long i = base + __popc(m & ((1u << lane) - 1u));
     base += __popc(m);
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(128) scene_fill_kernel(SceneCloudArgs a) {
       a.gidx[cell] = -1;
       continue;
     }
-    const double z = a.depth[(size_t)v * a.W + u];
+    const double z = a.depth[cell];
     const double x = (((double)u + 0.5) - a.cx) * z / a.fx;  // geometry.py:231
     const double y = (((double)v + 0.5) - a.cy) * z / a.fy;
     a.pts[3 * i] = x, a.pts[3 * i + 1] = y, a.pts[3 * i + 2] = z;
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(128) scene_fill_kernel(SceneCloudArgs a) {
     a.gidx[cell] = (int32_t)i;
     a.src[2 * i] = u, a.src[2 * i + 1] = v;
     a.cell[i] = (int32_t)cell;
-    a.labels_out[i] = a.labels[(size_t)v * a.W + u];  // raster.py:217
+    a.labels_out[i] = a.labels[cell];  // raster.py:217
     const double* c = a.color_grid + 3 * cell;
     double L, A, B;
     srgb_to_lab(c[0], c[1], c[2], L, A, B);
