@@ -1693,7 +1693,10 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
   PX_MARK();
   // 1, 2 or 4 warps per candidate: about two waves of 148 SMs x 24 warps when the batch is small
-  const int init_split = a.src.n >= 3552 ? 1 : (a.src.n >= 1776 ? 2 : 4);
+#ifndef PX_INIT_SPLIT_N
+#define PX_INIT_SPLIT_N 3552
+#endif
+  const int init_split = a.src.n >= 2 * PX_INIT_SPLIT_N ? 1 : (a.src.n >= PX_INIT_SPLIT_N ? 2 : 4);
   gicp_init_kernel<<<(unsigned)(((long long)a.src.n * init_split + 3) / 4), 128, smem_init, st>>>(a, init_split);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
@@ -1704,7 +1707,10 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
 #ifndef PX_NN_FILL
 #define PX_NN_FILL 4
 #endif
-  const int nn_split = (int)std::min<long long>(8, std::max<long long>(1, (148LL * 32 * PX_NN_FILL + a.src.n - 1) / a.src.n));
+#ifndef PX_NN_SPLIT_MAX
+#define PX_NN_SPLIT_MAX 8
+#endif
+  const int nn_split = (int)std::min<long long>(PX_NN_SPLIT_MAX, std::max<long long>(1, (148LL * 32 * PX_NN_FILL + a.src.n - 1) / a.src.n));
   for (int it = 1; it <= a.cfg.max_iter; ++it) {
     PX_MARK();
     gicp_nn_kernel<<<(unsigned)(((long long)a.src.n * nn_split + 3) / 4), 128, 0, st>>>(a, it, nn_split);
