@@ -324,3 +324,25 @@ def test_gicp_align_refuses_foreign_covariances(engine):
     with pytest.raises(DeviceError, match="covariances differ"):
         registration.gicp_align(src, tgt, ca * 1.5, cb, RigidTransform.identity(), cfg)
     assert registration.gicp_align(src, tgt, None, None, RigidTransform.identity(), cfg).iterations == res.iterations
+
+
+@pytest.mark.parametrize("stride", [1, 3])
+def test_other_strides_match_the_oracle(engine, stride):
+    """The device set-up path (observed cloud, lattice, targets, pruning windows) is not tied to stride 2: at
+    stride 1 and at a stride that does not divide the image size the public call returns the oracle's winners,
+    integer costs and (to 1e-4) poses, and the device-built observed cloud equals the host one."""
+    from paper_2008_00326_b200 import estimate_poses
+    d, frame, models, cfg, _ = G.scene("c1_box_3dof")
+    cfg = dataclasses.replace(cfg, stride=stride, dt=0.2 if stride > 1 else 0.4)
+    plan = plan_search(frame, models, cfg)
+    n = engine.upload_frame(frame, stride)
+    pts, lab, src, lbl = engine.download_scene_cloud(n)
+    assert n == len(plan.observed) and np.array_equal(pts, plan.observed.points) and np.array_equal(src, plan.observed.source_pixel)
+    assert np.array_equal(lbl, plan.obs_labels)
+    res = json.loads(result_to_json(estimate_poses(frame, models, cfg)))
+    ref = json.loads(result_to_json(assemble_result(plan, O.run_plan(frame, models, plan), 0.0)))
+    assert res["proposals_evaluated"] == ref["proposals_evaluated"] == plan.n
+    for a, b in zip(res["objects"], ref["objects"]):
+        assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
+        wt, wr = G.pose_delta(np.array(a["pose"]).reshape(3, 4), np.array(b["pose"]).reshape(3, 4))
+        assert wt <= 1e-4 and wr <= 1e-4
