@@ -346,3 +346,25 @@ def test_other_strides_match_the_oracle(engine, stride):
         assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
         wt, wr = G.pose_delta(np.array(a["pose"]).reshape(3, 4), np.array(b["pose"]).reshape(3, 4))
         assert wt <= 1e-4 and wr <= 1e-4
+
+
+def test_per_object_failures_through_the_device_path(engine):
+    """Per-object failures are data, not exceptions (search.py:237-251, reference tests/test_search.py:212-220):
+    an object whose mask holds no valid depth (6-DoF, `no_valid_depth`) and one without a model (`unknown_object`)
+    fail alone; the others are estimated exactly as the host-planned path estimates them."""
+    from paper_2008_00326_b200 import DepthImage, estimate_poses
+    d, frame, models, cfg, _ = G.scene("c4_mixed_6dof")
+    cfg = dataclasses.replace(cfg, viewpoints=6, n_inplane=2, max_proposals=None)
+    blind = int(frame.detections[0].object_id)
+    valid = frame.depth.valid & (frame.labels != blind)
+    frame2 = dataclasses.replace(frame, depth=DepthImage(frame.depth.values, valid))
+    gone = int(frame.detections[-1].object_id)
+    models2 = {o: m for o, m in models.items() if o != gone}
+    res = estimate_poses(frame2, models2, cfg)
+    by = {e.object_id: e for e in res.estimates}
+    assert by[blind].failed and by[blind].failure == "no_valid_depth"
+    assert by[gone].failed and by[gone].failure == "unknown_object"
+    assert sum(not e.failed for e in res.estimates) == len(res.estimates) - 2
+    flat = plan_search(frame2, models2, cfg)
+    want = assemble_result(flat, engine.run_plan(frame2, models2, flat), 0.0)
+    assert result_to_json(res) == result_to_json(want)
