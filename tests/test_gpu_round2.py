@@ -368,3 +368,33 @@ def test_per_object_failures_through_the_device_path(engine):
     flat = plan_search(frame2, models2, cfg)
     want = assemble_result(flat, engine.run_plan(frame2, models2, flat), 0.0)
     assert result_to_json(res) == result_to_json(want)
+
+
+def test_shards_without_candidates_and_empty_scenes(engine):
+    """Edge cases of the device set-up path: a rank that owns no grid cell (world size larger than the lattice)
+    contributes nothing and breaks nothing; a frame without a single valid depth pixel is scored like the
+    host-planned path scores it (every rendered point unexplained, no GICP target)."""
+    from paper_2008_00326_b200 import DepthImage, estimate_poses
+    from paper_2008_00326_b200.search import plan_lattice
+    d, frame, models, cfg, _ = G.scene("c1_box_3dof")
+    cfg = dataclasses.replace(cfg, dt=0.2)
+    lat = plan_lattice(frame, models, cfg)
+    engine.upload_frame(frame, cfg.stride)
+    engine.upload_models(models)
+    n_cells = lat.lattice[0].n_outer
+    assert engine.search_upload_lattice(lat, n_cells + 3, n_cells + 10) == 0      # owns nothing
+    engine.search_run(engine.search_cfg(lat))
+    engine.search_reduce()
+    assert engine.search_winners() == {}
+    assert engine.search_upload_lattice(lat, n_cells - 1, n_cells + 10) == lat.lattice[0].n_inner  # owns the last cell
+    engine.search_run(engine.search_cfg(lat))
+    engine.search_reduce()
+    w = engine.search_winners()
+    assert list(w) == [lat.active[0]] and (w[lat.active[0]][0] & 0xffffffff) // lat.lattice[0].n_inner == n_cells - 1
+    # no valid depth anywhere
+    dark = dataclasses.replace(frame, depth=DepthImage(frame.depth.values, np.zeros_like(frame.depth.valid)))
+    res = estimate_poses(dark, models, cfg)
+    flat = plan_search(dark, models, cfg)
+    want = assemble_result(flat, engine.run_plan(dark, models, flat), 0.0)
+    assert res.observed_points == 0 and result_to_json(res) == result_to_json(want)
+    assert all(e.cost.j_o == 0 and e.cost.j_r > 0 for e in res.estimates if not e.failed)
