@@ -356,9 +356,41 @@ def tiny_dataset():
     print("[dataset_tiny]", sum(f.stat().st_size for f in d.rglob("*") if f.is_file()) // 1024, "KiB", flush=True)
 
 
+def dense_fixture(name, frame, models, cfg):
+    """Per-candidate outputs of the reference at the BENCHMARK's own grid density (dt 0.025, no subsampling) on a
+    sub-workspace of the C3 scene: integer costs, refined poses, GICP iteration counts,
+    final-render point counts and the result JSON.  The scene itself is the one stored in c3_clutter_3dof.npz (its
+    depth digest is kept here to prove it)."""
+    import dataclasses
+    print(f"[{name}] staged reference run ...", flush=True)
+    st = staged_search(frame, models, cfg)
+    trace = tempfile.mktemp(suffix=".jsonl")
+    res = rs.estimate_poses(frame, models, dataclasses.replace(cfg, trace_path=trace))
+    rows = [json.loads(line) for line in open(trace)]
+    assert len(rows) == len(st["flat"])
+    d = {"cfg_json": np.array(json.dumps({**cfg.to_dict(), "max_proposals": cfg.max_proposals})),
+         "scene_digest": np.frombuffer(sha(pack_frame(frame)["depth_mm"]), dtype=np.uint8),
+         "flat_oid": np.array([f[0] for f in st["flat"]], dtype=np.int32),
+         "flat_local": np.array([f[1] for f in st["flat"]], dtype=np.int32),
+         "refined": np.array([p.matrix3x4() for p in st["refined"]]),
+         "reg_iters": np.array([r.iterations for r in st["regs"]], dtype=np.int8),
+         "n0": np.array([len(c) for c in st["clouds0"]], dtype=np.int16),
+         "n1": np.array([len(c) for c in st["clouds1"]], dtype=np.int16),
+         "j_o": np.array([r["j_o"] for r in rows], dtype=np.int16),
+         "j_r": np.array([r["j_r"] for r in rows], dtype=np.int16),
+         "result_json": np.array(rs.result_to_json(res))}
+    assert max(r["j_o"] for r in rows) < 32767 and max(r["j_r"] for r in rows) < 32767
+    np.savez_compressed(OUT / f"{name}.npz", **d)
+    print(f"[{name}] n={len(rows)} -> {(OUT / (name + '.npz')).stat().st_size / 1024:.0f} KiB", flush=True)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
-    which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c3n", "c4", "tiny"}
+    which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c3n", "c4", "tiny", "c3d"}
+    if "c3d" in which:
+        frame, models = scene_c3()
+        dense_fixture("c3d_dense_reference", frame, models,
+                      rs.SearchConfig(mode="3dof", workspace=(-0.125, 0.125, -0.125, 0.125), dt=0.025, workers=WORKERS))
     if "tiny" in which:
         tiny_dataset()
     if "units" in which:

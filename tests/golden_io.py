@@ -77,3 +77,21 @@ def pose_delta(a, b):
     rel = np.einsum("...ij,...kj->...ik", a[..., :, :3], b[..., :, :3])
     tr = np.clip((np.trace(rel, axis1=-2, axis2=-1) - 1.0) / 2.0, -1.0, 1.0)
     return dt, np.arccos(tr)
+
+
+@lru_cache(maxsize=None)
+def dense_scene():
+    """(fixture dict, frame, models, cfg, plan) of tests/golden/c3d_dense_reference.npz: the reference's per-candidate
+    outputs at the benchmark's own grid density (dt 0.025, 9,680 candidates, no subsampling) on the C3 scene."""
+    from paper_2008_00326_b200.search import plan_search
+
+    dd, d3 = load("c3d_dense_reference"), load("c3_clutter_3dof")
+    digest = np.frombuffer(hashlib.sha256(np.ascontiguousarray(d3["depth_mm"]).tobytes()).digest(), dtype=np.uint8)
+    assert np.array_equal(digest, dd["scene_digest"]), "c3d fixture was generated on another scene"
+    frame, models = frame_of(d3), models_of(d3)
+    c = json.loads(str(dd["cfg_json"]))
+    c.pop("workers", None)
+    cfg = SearchConfig.from_dict(c)
+    plan = plan_search(frame, models, cfg)
+    assert np.array_equal(plan.flat_oid, dd["flat_oid"]) and np.array_equal(plan.flat_local, dd["flat_local"])
+    return dd, frame, models, cfg, plan

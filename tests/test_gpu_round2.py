@@ -398,3 +398,34 @@ def test_shards_without_candidates_and_empty_scenes(engine):
     want = assemble_result(flat, engine.run_plan(dark, models, flat), 0.0)
     assert res.observed_points == 0 and result_to_json(res) == result_to_json(want)
     assert all(e.cost.j_o == 0 and e.cost.j_r > 0 for e in res.estimates if not e.failed)
+
+
+# candidates of the dense fixture on which device and reference part ways (chaotic GICP iterates)
+DENSE_CHAOTIC_DEVICE = {1813, 1821, 9555, 9563, 9566}
+
+
+def test_device_at_benchmark_density_against_the_reference(engine):
+    """The CUDA path against the REFERENCE ITSELF (not the port) at the benchmark's own grid density: 9,680 candidates of
+    the C3 scene (dt 0.025, no subsampling; tests/golden/c3d_dense_reference.npz).  First / final render counts, GICP
+    iteration counts, both integer costs and the refined pose (1e-4 m / 1e-4 rad) of every candidate except the
+    chaotic few named above; per-object winners; and the public call's JSON."""
+    from paper_2008_00326_b200 import estimate_poses
+    dd, frame, models, cfg, plan = G.dense_scene()
+    out = engine.run_plan(frame, models, plan)
+    assert np.array_equal(out.n_first, dd["n0"])
+    dt, dr = G.pose_delta(out.refined_cam, dd["refined"])
+    close = (dt <= 1e-4) & (dr <= 1e-4)
+    same = (out.j_o == dd["j_o"]) & (out.j_r == dd["j_r"])
+    bad = sorted(set(np.nonzero(~close)[0].tolist()) | set(np.nonzero(~same)[0].tolist()))
+    print(f"dense: n={plan.n} poses within tol {close.mean():.5f}, costs equal {same.mean():.5f}, divergent {bad}")
+    assert set(bad) <= DENSE_CHAOTIC_DEVICE
+    ok = np.ones(plan.n, bool)
+    ok[sorted(DENSE_CHAOTIC_DEVICE)] = False
+    assert np.array_equal(out.iterations[ok], dd["reg_iters"][ok]) and np.array_equal(out.n_rendered[ok], dd["n1"][ok])
+    ref = json.loads(str(dd["result_json"]))
+    for got in (json.loads(result_to_json(assemble_result(plan, out, 0.0))), json.loads(result_to_json(estimate_poses(frame, models, cfg)))):
+        assert got["proposals_evaluated"] == ref["proposals_evaluated"] == 9680
+        for a, b in zip(ref["objects"], got["objects"]):
+            assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
+            wt, wr = G.pose_delta(np.array(a["pose"]).reshape(3, 4), np.array(b["pose"]).reshape(3, 4))
+            assert wt <= 1e-4 and wr <= 1e-4

@@ -232,3 +232,30 @@ def test_gicp_weights_are_not_bit_symmetric_at_a_general_pose():
     asym = (w != np.transpose(w, (0, 2, 1))).any(axis=(1, 2))
     assert nc > 50 and asym.mean() > 0.5
     assert np.abs(w - np.transpose(w, (0, 2, 1))).max() < 1e-9 * np.abs(w).max()  # symmetric as a matrix, not as bits
+
+
+def test_oracle_at_benchmark_density_against_the_reference():
+    """9,680 candidates of the C3 scene at the benchmark's own grid density (dt 0.025, no subsampling), the reference's
+    per-candidate outputs (tests/golden/c3d_dense_reference.npz): first / final render counts and GICP iteration
+    counts; integer costs and refined poses (1e-4 m / 1e-4 rad) for every candidate
+    but the chaotic few named below; per-object winners."""
+    dd, frame, models, cfg, plan = G.dense_scene()
+    out = O.run_plan(frame, models, plan, n_threads=8)
+    assert np.array_equal(out.n_first, dd["n0"])
+    dt, dr = G.pose_delta(out.refined_cam, dd["refined"])
+    close = (dt <= 1e-4) & (dr <= 1e-4)
+    same = (out.j_o == dd["j_o"]) & (out.j_r == dd["j_r"])
+    bad = sorted(set(np.nonzero(~close)[0].tolist()) | set(np.nonzero(~same)[0].tolist()))
+    print(f"dense: n={plan.n} poses within tol {close.mean():.5f}, costs equal {same.mean():.5f}, divergent {bad}")
+    assert set(bad) <= DENSE_CHAOTIC_ORACLE
+    ok = np.ones(plan.n, bool)
+    ok[sorted(DENSE_CHAOTIC_ORACLE)] = False
+    assert np.array_equal(out.iterations[ok], dd["reg_iters"][ok]) and np.array_equal(out.n_rendered[ok], dd["n1"][ok])
+    ref = json.loads(str(dd["result_json"]))
+    mine = json.loads(result_to_json(assemble_result(plan, out, 0.0)))
+    for a, b in zip(ref["objects"], mine["objects"]):
+        assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
+
+
+# candidates on which the reference (LAPACK / libm) and the restated arithmetic part ways (SURVEY 7.3 H4): 5 of 9,680
+DENSE_CHAOTIC_ORACLE = {1813, 1821, 9555, 9563, 9566}
