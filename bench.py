@@ -373,7 +373,9 @@ def run_gpu(args):
     # ---- per-scene latency and multi-scene batching on the small config (BASELINE: "per-scene latency") ----
     latency = None
     if world == 1 and not args.no_latency:
+        lat_sampler = ClockSampler(local)
         latency = small_scene_latency(eng)
+        latency["clocks"] = lat_sampler.stop()
 
     # ---- CPU baseline on a bounded sample of the same workload (rank 0, N=1 only) ----
     cpu = None
@@ -404,6 +406,7 @@ def run_gpu(args):
                 "estimate_poses_value": (n_total / (api_ms * 1e-3)) if api_ms else None},
         "gpu_launches": int(launches),
         "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "latency": latency,
+        "latency_ms": latency["estimate_poses_ms"] if latency else None,  # C1 (1,936 candidates): one public call, host to host
         "mean_iterations": float(full.iterations.mean()), "mean_rendered_points": float(full.n_rendered.mean()),
     }
     print(json.dumps(line))
