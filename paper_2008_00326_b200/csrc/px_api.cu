@@ -88,7 +88,7 @@ struct px_ctx {
   int tgt_k = 0;
   double tgt_gate = 0.0, tgt_eps = 0.0;
   DevBuf tgt_v0, tgt_obs, tgt_world, tgt_sizes, tgt_scans, tgt_params,
-         tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lstart, tgt_lpts;
+         tgt_off, tgt_pts, tgt_cov, tgt_soa, tgt_org, tgt_map, tgt_pix, tgt_boxes, tgt_lpts;
   bool tgt_organised = false;
   double tgt_rot[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};  // TargetsDev::rot of the resident targets
   bool tgt_obs_valid = false;  // tgt_obs holds the observed indices of the resident targets (device-built)
@@ -426,7 +426,7 @@ void px_ctx_destroy(px_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->depth, &ctx->valid, &ctx->labels, &ctx->obs_pts, &ctx->obs_lab, &ctx->obs_labels,
                     &ctx->gx, &ctx->gy, &ctx->gz, &ctx->gidx, &ctx->models_dev, &ctx->label_count,
                     &ctx->obs_cell, &ctx->tgt_v0, &ctx->tgt_obs, &ctx->tgt_world, &ctx->tgt_sizes, &ctx->tgt_scans, &ctx->tgt_params,
-                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lstart, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
+                    &ctx->tgt_off, &ctx->tgt_pts, &ctx->tgt_cov, &ctx->tgt_soa, &ctx->tgt_org, &ctx->tgt_map, &ctx->tgt_pix, &ctx->tgt_boxes, &ctx->tgt_lpts, &ctx->c_slot, &ctx->c_pose, &ctx->c_tidx,
                     &ctx->c_rank, &ctx->src_cov, &ctx->w_buf, &ctx->corr, &ctx->nn, &ctx->st_pose, &ctx->st_i, &ctx->st_hg, &ctx->total_dev, &ctx->r_T,
                     &ctx->r_iters, &ctx->r_flags, &ctx->r_pose, &ctx->r_jo, &ctx->r_jr, &ctx->r_nfirst,
                     &ctx->r_nfinal, &ctx->r_key, &ctx->bitmap, &ctx->r_ncorr, &ctx->r_cap0, &ctx->r_cap1, &ctx->r_nm, &ctx->r_nfp};
@@ -857,7 +857,6 @@ static TargetsDev targets_dev(px_ctx* ctx) {
   t.org = ctx->tgt_organised ? ctx->tgt_org.as<TgtOrg>() : nullptr;
   t.tmap = ctx->tgt_map.as<int32_t>();
   t.boxes32 = ctx->tgt_boxes.as<float>();
-  t.leaf_start = ctx->tgt_lstart.as<int32_t>();
   t.leaf32 = ctx->tgt_lpts.as<float4>();
   t.soa = ctx->tgt_soa.as<double>();
   t.plane = std::max<long long>(ctx->tgt_total, 1);
@@ -894,7 +893,6 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   std::vector<int32_t> tmap, tpix;
   std::vector<double> boxes;   // {lo xyz, hi xyz} per node, converted to fp32 centre/half-extent below
   std::vector<float> boxes32, leaf32;
-  std::vector<int32_t> lstart;
   if (org) {
     const int st = ctx->cam.stride;
     tpix.resize((size_t)total);
@@ -948,49 +946,24 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
             }
         }
       }
-      // leaf arrays: every target's points grouped by block (ascending local index inside a block)
-      lstart.assign((size_t)(box_total + n_targets), 0);
-      leaf32.resize((size_t)total * 4);
-      for (int t = 0; t < n_targets; ++t) {
-        const TgtOrg& o = orgs[(size_t)t];
-        const long long a = off[(size_t)t], b = off[(size_t)t + 1];
-        const int nb_ = o.bw * o.bh;
-        int32_t* ls = lstart.data() + o.box_off + t;
-        std::vector<int32_t> cnt((size_t)nb_ + 1, 0);
-        auto blk = [&](long long i) {
-          const int cell = tpix[(size_t)i];
-          return ((cell / o.w) / PX_BLK) * o.bw + (cell % o.w) / PX_BLK;
-        };
-        for (long long i = a; i < b; ++i) cnt[(size_t)blk(i) + 1]++;
-        for (int q = 0; q < nb_; ++q) cnt[(size_t)q + 1] += cnt[(size_t)q];
-        for (int q = 0; q <= nb_; ++q) ls[q] = cnt[(size_t)q];
-        for (long long i = a; i < b; ++i) {
-          const int k = cnt[(size_t)blk(i)]++;
-          for (int d = 0; d < 3; ++d) leaf32[(size_t)(4 * (a + k) + d)] = (float)points[3 * i + d];
-          const int32_t li = (int32_t)(i - a);
-          memcpy(&leaf32[(size_t)(4 * (a + k) + 3)], &li, 4);
-        }
-      }
     }
   }
   if (org) {
-    // fp32 pruning copies: centre / half-extent with the half-extent inflated by the centre's
-    // rounding (rounded up), and the per-target bound `err` on all fp32 rounding in the tests.
-    // Device layout per target (TgtOrg::box_off counts 6-float nodes; 17 per super-block): for every
-    // super-block six planes {cx, cy, cz, hx, hy, hz} x 16 blocks (row-major inside the super-block,
-    // blocks outside the map are empty boxes), then the super-blocks' own {c, h} x 3.
-    auto conv = [](const double* b6, float* c3, float* h3, int stride) {
+    // fp32 pruning copies: lo rounded down / hi rounded up (the fp32 box contains the exact one), and the per-target
+    // bound `err` on all fp32 rounding in the tests.  Device layout per target (TgtOrg::box_off counts nodes; 17 per
+    // super-block): for every super-block six planes {lox, loy, loz, hix, hiy, hiz} x 16 block slots (row-major
+    // inside the super-block, slots outside the map are empty boxes), then the super-blocks' own {lo, hi}; and one
+    // leaf record per block slot: planes x[16], y[16], z[16] over the block's 4x4 map cells (PX_FAR32 = no point).
+    auto conv = [](const double* b6, float* lo3, float* hi3, int stride) {
       for (int d = 0; d < 3; ++d) {
         const double lo = b6[d], hi = b6[3 + d];
-        float cf = 0.f, hf = -1e30f;  // empty node: distance overflows to +inf and is always pruned
+        float lf = PX_FAR32, hf = -PX_FAR32;  // empty node: distance overflows to +inf and is always pruned
         if (lo <= hi) {
-          const double c = 0.5 * (lo + hi);
-          cf = (float)c;
-          const double h = std::max(hi - (double)cf, (double)cf - lo);
-          hf = (float)h;
-          if ((double)hf < h) hf = std::nextafterf(hf, INFINITY);
+          lf = (float)lo, hf = (float)hi;
+          if ((double)lf > lo) lf = std::nextafterf(lf, -INFINITY);
+          if ((double)hf < hi) hf = std::nextafterf(hf, INFINITY);
         }
-        c3[d * stride] = cf, h3[d * stride] = hf;
+        lo3[d * stride] = lf, hi3[d * stride] = hf;
       }
     };
     long long node_total = 0;
@@ -1001,13 +974,14 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
       node_total += 17 * ns + (ns & 1);  // even: keeps every target's planes 16-byte aligned
     }
     boxes32.assign((size_t)node_total * 6, 0.f);
-    std::vector<int32_t> lstart2((size_t)(node_total + n_targets), 0);
+    leaf32.assign((size_t)node_total * 48, PX_FAR32);
     const double empty6[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
     for (int t = 0; t < n_targets; ++t) {
       TgtOrg& o = orgs[(size_t)t];
       const double* bbd = boxes.data() + 6 * o.box_off;
       const double* sbd = bbd + 6 * (long long)o.bw * o.bh;
       float* out = boxes32.data() + 6 * new_off[(size_t)t];
+      float* recs = leaf32.data() + 48 * new_off[(size_t)t];
       const int ns = o.sw * o.sh;
       for (int s_ = 0; s_ < ns; ++s_) {
         float* blk = out + 96 * (size_t)s_;
@@ -1019,12 +993,16 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
         float* sbo = out + 96 * (size_t)ns + 6 * (size_t)s_;
         conv(sbd + 6 * s_, sbo, sbo + 3, 1);
       }
-      // leaf starts move with the node numbering
-      const int nb_ = o.bw * o.bh;
-      for (int q = 0; q <= nb_; ++q) lstart2[(size_t)(new_off[(size_t)t] + t + q)] = lstart[(size_t)(o.box_off + t + q)];
+      for (long long i = off[(size_t)t]; i < off[(size_t)t + 1]; ++i) {
+        const int cell = tpix[(size_t)i], x = cell % o.w, y = cell / o.w;
+        const int bx = x / PX_BLK, by = y / PX_BLK;
+        const int s_ = (by / PX_BLK) * o.sw + bx / PX_BLK, q = (by % PX_BLK) * PX_BLK + bx % PX_BLK;
+        float* rec = recs + 48 * ((size_t)16 * s_ + q);
+        const int c = (y % PX_BLK) * PX_BLK + x % PX_BLK;
+        for (int d = 0; d < 3; ++d) rec[16 * d + c] = (float)points[3 * i + d];
+      }
       o.box_off = new_off[(size_t)t];
     }
-    lstart.swap(lstart2);
     for (int t = 0; t < n_targets; ++t) {
       double m = 0.0;
       for (long long i = off[(size_t)t]; i < off[(size_t)t + 1]; ++i)
@@ -1045,7 +1023,6 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     if (int r = h2d(ctx, ctx->tgt_map, tmap.data(), tmap.size() * 4)) return r;
     if (int r = h2d(ctx, ctx->tgt_pix, tpix.data(), tpix.size() * 4)) return r;
     if (int r = h2d(ctx, ctx->tgt_boxes, boxes32.data(), boxes32.size() * 4)) return r;
-    if (int r = h2d(ctx, ctx->tgt_lstart, lstart.data(), lstart.size() * 4)) return r;
     if (int r = h2d(ctx, ctx->tgt_lpts, leaf32.data(), leaf32.size() * 4)) return r;
   }
   const size_t tot1 = (size_t)std::max<long long>(total, 1);
@@ -1134,14 +1111,13 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   CU(ctx->tgt_pix.ensure(tot1 * 4));
   CU(ctx->tgt_map.ensure((size_t)std::max<long long>(totals[1], 1) * 4));
   CU(ctx->tgt_boxes.ensure((size_t)std::max<long long>(totals[2], 1) * 24));
-  CU(ctx->tgt_lstart.ensure((size_t)(totals[2] + n + 1) * 4));
-  CU(ctx->tgt_lpts.ensure(tot1 * 16));
+  CU(ctx->tgt_lpts.ensure((size_t)std::max<long long>(totals[2], 1) * 192));
   CU(ctx->tgt_cov.ensure(tot1 * 72));
   CU(ctx->tgt_v0.ensure(tot1 * 24));
   CU(ctx->tgt_soa.ensure(tot1 * 72));
   a.tgt_obs = ctx->tgt_obs.as<int32_t>(), a.tgt_pts = ctx->tgt_pts.as<double>(), a.tpix = ctx->tgt_pix.as<int32_t>();
   a.tmap = ctx->tgt_map.as<int32_t>(), a.boxes32 = ctx->tgt_boxes.as<float>();
-  a.leaf_start = ctx->tgt_lstart.as<int32_t>(), a.leaf32 = ctx->tgt_lpts.as<float4>();
+  a.leaf32 = ctx->tgt_lpts.as<float4>();
   ctx->tgt_organised = true, ctx->tgt_obs_valid = true;
   ctx->n_targets = n, ctx->tgt_total = total, ctx->tgt_k = k, ctx->tgt_gate = cfg->max_correspondence_distance;
   ctx->tgt_eps = cfg->epsilon;

@@ -394,16 +394,58 @@ __device__ __forceinline__ double box_dist2(const double* __restrict__ b, double
   return dx * dx + dy * dy + dz * dz;
 }
 
-// fp32 squared distance from a point to a box stored as centre / half-extent; the
-// half-extents were inflated on the host so that this never exceeds the exact
-// squared distance to any member point by more than the threshold slack.
+// fp32 squared distance from a point to a box stored as {lo xyz, hi xyz}; lo was rounded down and hi up when the
+// box was converted, so the fp32 box contains the exact one and this never exceeds the exact squared distance to
+// any member point by more than the threshold slack.
 __device__ __forceinline__ float box_dist2f(const float* __restrict__ b, float qx, float qy, float qz) {
   const float2 b0 = __ldg(reinterpret_cast<const float2*>(b)), b1 = __ldg(reinterpret_cast<const float2*>(b) + 1),
                b2 = __ldg(reinterpret_cast<const float2*>(b) + 2);
-  const float gx = fmaxf(fabsf(qx - b0.x) - b1.y, 0.f);
-  const float gy = fmaxf(fabsf(qy - b0.y) - b2.x, 0.f);
-  const float gz = fmaxf(fabsf(qz - b1.x) - b2.y, 0.f);
+  const float gx = fmaxf(fmaxf(b0.x - qx, qx - b1.y), 0.f);
+  const float gy = fmaxf(fmaxf(b0.y - qy, qy - b2.x), 0.f);
+  const float gz = fmaxf(fmaxf(b1.x - qz, qz - b2.y), 0.f);
   return fmaf(gz, gz, fmaf(gy, gy, gx * gx));
+}
+
+// Blackwell's two-wide fp32 arithmetic (FADD2 / FMUL2 / FFMA2: one issue slot for two IEEE-rounded results) on
+// register pairs; the pruning tests below run on pairs of boxes / pairs of leaf points.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) { asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v)); }
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// squared distances of a query to two boxes {lo, hi} (per axis: max(lo - q, q - hi, 0)), two-wide
+__device__ __forceinline__ f32x2 box_pair_dist2(f32x2 lx, f32x2 ly, f32x2 lz, f32x2 hx, f32x2 hy, f32x2 hz, f32x2 qx,
+                                                f32x2 qy, f32x2 qz) {
+  float a0, a1, b0, b1;
+  upk2(sub2(lx, qx), a0, a1), upk2(sub2(qx, hx), b0, b1);
+  const f32x2 gx = pk2(fmaxf(fmaxf(a0, b0), 0.f), fmaxf(fmaxf(a1, b1), 0.f));
+  upk2(sub2(ly, qy), a0, a1), upk2(sub2(qy, hy), b0, b1);
+  const f32x2 gy = pk2(fmaxf(fmaxf(a0, b0), 0.f), fmaxf(fmaxf(a1, b1), 0.f));
+  upk2(sub2(lz, qz), a0, a1), upk2(sub2(qz, hz), b0, b1);
+  const f32x2 gz = pk2(fmaxf(fmaxf(a0, b0), 0.f), fmaxf(fmaxf(a1, b1), 0.f));
+  return fma2(gz, gz, fma2(gy, gy, mul2(gx, gx)));
+}
+// squared distances of a query to two points, two-wide
+__device__ __forceinline__ f32x2 pt_pair_dist2(f32x2 x, f32x2 y, f32x2 z, f32x2 qx, f32x2 qy, f32x2 qz) {
+  const f32x2 tx = sub2(x, qx), ty = sub2(y, qy), tz = sub2(z, qz);
+  return fma2(tz, tz, fma2(ty, ty, mul2(tx, tx)));
 }
 
 // Lexicographic minimum of (d2, index) over the target points with d2 <= gate2,
@@ -448,63 +490,75 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
     const float qxf = (float)(T.rot[0] * qx + T.rot[1] * qy + T.rot[2] * qz);
     const float qyf = (float)(T.rot[3] * qx + T.rot[4] * qy + T.rot[5] * qz);
     const float qzf = (float)(T.rot[6] * qx + T.rot[7] * qy + T.rot[8] * qz);
-    const int32_t* lstart = T.leaf_start + o.box_off + ti;  // (bw*bh + 1) entries per target
-    const float4* lp = T.leaf32 + toff;                     // points grouped by block: {x, y, z, index bits}
-    // boxes: per super-block six planes {cx,cy,cz,hx,hy,hz} x 16 block slots, then the super-blocks' {c,h}
+    const int32_t* map = T.tmap + o.map_off;
+    // boxes: per super-block six planes {lox,loy,loz,hix,hiy,hiz} x 16 block slots, then the super-blocks' {lo, hi};
+    // leaves: one fixed record per block slot, three planes {x, y, z} x 16 map cells of the block (row-major;
+    // cells without a point hold a far-away sentinel), so a leaf is 12 vector loads and 8 two-wide distance
+    // evaluations without loop control; the local index of a survivor comes from the pixel map
     const float* bb = T.boxes32 + 6 * o.box_off;
     const float* sb = bb + 96 * (long long)o.sw * o.sh;
+    const ulonglong2* leaves = reinterpret_cast<const ulonglong2*>(T.leaf32) + 12 * o.box_off;
+    const f32x2 QX = pk2(qxf, qxf), QY = pk2(qyf, qyf), QZ = pk2(qzf, qzf);
     for (int sy = 0; sy < o.sh; ++sy)
       for (int sx = 0; sx < o.sw; ++sx) {
         NN_STAT(2, 1);
-        if (box_dist2f(sb + 6 * (sy * o.sw + sx), qxf, qyf, qzf) > thr) continue;
+        const int sbi = sy * o.sw + sx;
+        if (box_dist2f(sb + 6 * sbi, qxf, qyf, qzf) > thr) continue;
         // phase 1: test the 16 block slots of this super-block back to back -- vector loads, independent
         // arithmetic, no control flow (slots outside the map hold empty boxes) -- survivors into a bit mask
-        const int bx0 = sx * PX_BLK, by0 = sy * PX_BLK;
-        const float4* pl = reinterpret_cast<const float4*>(bb + 96 * (sy * o.sw + sx));
+        const ulonglong2* pl = reinterpret_cast<const ulonglong2*>(bb + 96 * sbi);
         unsigned bmask = 0;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          const float4 cx = __ldg(pl + g), cy = __ldg(pl + 4 + g), cz = __ldg(pl + 8 + g);
-          const float4 hx = __ldg(pl + 12 + g), hy = __ldg(pl + 16 + g), hz = __ldg(pl + 20 + g);
-#define PX_BT(e, bit)                                                                  \
-  {                                                                                    \
-    const float gx = fmaxf(fabsf(qxf - cx.e) - hx.e, 0.f);                             \
-    const float gy = fmaxf(fabsf(qyf - cy.e) - hy.e, 0.f);                             \
-    const float gz = fmaxf(fabsf(qzf - cz.e) - hz.e, 0.f);                             \
-    bmask |= (unsigned)!(fmaf(gz, gz, fmaf(gy, gy, gx * gx)) > thr) << (4 * g + bit);  \
-  }
-          PX_BT(x, 0) PX_BT(y, 1) PX_BT(z, 2) PX_BT(w, 3)
-#undef PX_BT
+          const ulonglong2 lx = __ldg(pl + g), ly = __ldg(pl + 4 + g), lz = __ldg(pl + 8 + g);
+          const ulonglong2 hx = __ldg(pl + 12 + g), hy = __ldg(pl + 16 + g), hz = __ldg(pl + 20 + g);
+          float d0, d1, d2_, d3;
+          upk2(box_pair_dist2(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, QX, QY, QZ), d0, d1);
+          upk2(box_pair_dist2(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, QX, QY, QZ), d2_, d3);
+          if (!(d0 > thr)) bmask |= 1u << (4 * g);
+          if (!(d1 > thr)) bmask |= 2u << (4 * g);
+          if (!(d2_ > thr)) bmask |= 4u << (4 * g);
+          if (!(d3 > thr)) bmask |= 8u << (4 * g);
         }
         NN_STAT(3, PX_BLK * PX_BLK);
         while (bmask) {
           const int q = __ffs(bmask) - 1;
           bmask &= bmask - 1;
-          const int b = (by0 + (q >> 2)) * o.bw + bx0 + (q & 3);
-          const int k0 = lstart[b], k1 = lstart[b + 1];
-          NN_STAT(4, k1 - k0);
+          NN_STAT(4, 16);
           NN_STAT(6, 1);
-          // phase 1 over the leaf (<= 16 points): fp32 squared distances, survivors into a mask
+          // phase 1 over the leaf record (16 cells): fp32 squared distances two at a time, survivors into a mask
+          const ulonglong2* lr = leaves + 12 * (16 * sbi + q);
           unsigned pmask = 0;
-#pragma unroll 4
-          for (int k = k0; k < k1; ++k) {
-            const float4 pf = __ldg(lp + k);
-            const float tx = pf.x - qxf, ty = pf.y - qyf, tz = pf.z - qzf;
-            pmask |= (unsigned)!(fmaf(tz, tz, fmaf(ty, ty, tx * tx)) > thr) << (k - k0);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const ulonglong2 X = __ldg(lr + g), Y = __ldg(lr + 4 + g), Z = __ldg(lr + 8 + g);
+            float d0, d1, d2_, d3;
+            upk2(pt_pair_dist2(X.x, Y.x, Z.x, QX, QY, QZ), d0, d1);
+            upk2(pt_pair_dist2(X.y, Y.y, Z.y, QX, QY, QZ), d2_, d3);
+            if (!(d0 > thr)) pmask |= 1u << (4 * g);
+            if (!(d1 > thr)) pmask |= 2u << (4 * g);
+            if (!(d2_ > thr)) pmask |= 4u << (4 * g);
+            if (!(d3 > thr)) pmask |= 8u << (4 * g);
           }
           // phase 2: exact fp64 evaluation of the few survivors, reference operation order
-          bool improved = false;
-          while (pmask) {
-            const int k = k0 + __ffs(pmask) - 1;
-            pmask &= pmask - 1;
-            const int j = __float_as_int(__ldg(&lp[k].w));
-            const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
-            const double d2 = dx * dx + dy * dy + dz * dz;
-            if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;
-          }
-          if (improved) thr = nn_threshold(best, o.err);
+          if (pmask) {
+            const int cell0 = ((sy * PX_BLK + (q >> 2)) * PX_BLK) * o.w + (sx * PX_BLK + (q & 3)) * PX_BLK;
+            bool improved = false;
+            do {
+              const int k = __ffs(pmask) - 1;
+              pmask &= pmask - 1;
+              const int j = __ldg(map + cell0 + (k >> 2) * o.w + (k & 3));
+              const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
+              const double d2 = dx * dx + dy * dy + dz * dz;
+              if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;
+            } while (pmask);
+            if (improved) thr = nn_threshold(best, o.err);
 #ifdef PX_NN_STATS
-          ++n_leaves_, n_improved_ += improved;
+            n_improved_ += improved;
+#endif
+          }
+#ifdef PX_NN_STATS
+          ++n_leaves_;
 #endif
         }
       }

@@ -89,11 +89,12 @@ struct CloudsDev {
 // PX_BLK block of map cells (bh x bw of them) followed by those of every PX_BLK x
 // PX_BLK group of blocks (sh x sw).
 #define PX_BLK 4
+#define PX_FAR32 1e30f  // coordinate of an absent leaf point / bound of an empty box: every distance to it overflows to +inf
 struct TgtOrg {
   int gx0, gy0, w, h;
   int bw, bh, sw, sh;
   long long map_off;
-  long long box_off;  // in boxes32 (units of 6 floats) / leaf_start
+  long long box_off;  // first node of the target in boxes32 (units of 6 floats) / leaf32 (units of 48 floats)
   double err;         // bound on every fp32 rounding error of the pruning tests for this target (metres)
 };
 
@@ -104,9 +105,9 @@ struct TargetsDev {
   const double* cov;        // (sum,9)
   const TgtOrg* org;        // (n_targets) or null
   const int32_t* tmap;
-  const float* boxes32;       // per node {cx,cy,cz,hx,hy,hz}: fp32 centre / inflated half-extent of the 3-D box
-  const int32_t* leaf_start;  // per target bw*bh+1 entries at [box_off + target index]
-  const float4* leaf32;       // (sum) points grouped by block: fp32 copy {x,y,z} + local index bits
+  const float* boxes32;       // per node {lo xyz, hi xyz}: fp32 3-D box, lo rounded down / hi rounded up (SoA per super-block)
+  const float4* leaf32;       // per block slot (node numbering of boxes32): fp32 planes x[16], y[16], z[16] of the block's
+                              //   4x4 map cells (row-major; PX_FAR32 where the cell holds no point) -- 12 float4 = 192 B
   const double* soa;          // 6 planes of `plane` doubles: x, y, z and the normal v0 the covariance I - f v0 v0^T is
   long long plane;            //   made of -- coherent-gather copy for the linearise kernel, which rebuilds the matrix
   double f;                   // 1 - epsilon the target covariances were built with
@@ -152,8 +153,7 @@ struct TgtBuildArgs {
   int32_t* tpix;              // (sum) map cell
   int32_t* tmap;              // (sum cells), -1 on entry
   float* boxes32;             // (sum nodes,6)
-  int32_t* leaf_start;        // (sum nodes + n)
-  float4* leaf32;             // (sum)
+  float4* leaf32;             // (sum nodes,12)
 };
 cudaError_t launch_tgt_world(const TgtBuildArgs& a, cudaStream_t st);
 cudaError_t launch_tgt_count(const TgtBuildArgs& a, cudaStream_t st);

@@ -8,7 +8,7 @@
 // world-frame point is `p @ R.T + t` in the host BLAS order, px_common.cuh) and compacts the
 // survivors in ascending observed index, which is the order np.nonzero returns.  The organised
 // views the nearest-neighbour search needs (pixel map, two-level box hierarchy, per-block leaf
-// arrays, fp32 error bound) are built here as well, with the rules px_targets_upload applies on
+// records, fp32 error bound) are built here as well, with the rules px_targets_upload applies on
 // the host -- tests compare both paths bit for bit.
 #include "px_kernels.h"
 
@@ -179,97 +179,58 @@ __global__ void __launch_bounds__(256) tgt_fill_kernel(TgtBuildArgs a) {
   }
 }
 
-// fp32 pruning copy of a box: centre / half-extent, the half-extent inflated by the centre's rounding
-__device__ __forceinline__ void box32(const double* lo, const double* hi, float* c3, float* h3, int stride) {
+// fp32 pruning copy of a box: lo rounded down, hi rounded up (the fp32 box contains the exact one); an empty node gets
+// an inverted far-away box whose distance overflows to +inf and is always pruned
+__device__ __forceinline__ void box32(const double* lo, const double* hi, float* lo3, float* hi3, int stride) {
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    float cf = 0.f, hf = -1e30f;  // empty node: distance overflows to +inf and is always pruned
-    if (lo[d] <= hi[d]) {
-      const double c = 0.5 * (lo[d] + hi[d]);
-      cf = (float)c;
-      const double h = fmax(hi[d] - (double)cf, (double)cf - lo[d]);
-      hf = (float)h;
-      if ((double)hf < h) hf = nextafterf(hf, CUDART_INF_F);
-    }
-    c3[d * stride] = cf, h3[d * stride] = hf;
+    float lf = PX_FAR32, hf = -PX_FAR32;
+    if (lo[d] <= hi[d]) lf = __double2float_rd(lo[d]), hf = __double2float_ru(hi[d]);
+    lo3[d * stride] = lf, hi3[d * stride] = hf;
   }
 }
 
-// pass 3: per target, boxes of every block / super-block, leaf start offsets and leaf arrays
+// pass 3: per target, boxes of every block / super-block and the fixed-size leaf record of every block slot
 __global__ void __launch_bounds__(256) tgt_tree_kernel(TgtBuildArgs a) {
   const int t = blockIdx.x;
   const TgtOrg o = a.org[t];
   const long long off = a.offset[t];
   const int32_t* map = a.tmap + o.map_off;
   const double* P = a.tgt_pts + 3 * off;
-  const int nb = o.bw * o.bh, ns = o.sw * o.sh;
+  const int ns = o.sw * o.sh;
   float* bb = a.boxes32 + 6 * o.box_off;  // per super-block 6 planes x 16 block slots, then the super-block nodes
-  int32_t* ls = a.leaf_start + o.box_off + t;
-  // boxes (a thread per block slot / super-block scans the node's map cells)
+  float* leaves = reinterpret_cast<float*>(a.leaf32) + 48 * o.box_off;  // per block slot: x[16], y[16], z[16] by map cell
+  // a thread per block slot / super-block scans the node's map cells
   for (int q = threadIdx.x; q < 17 * ns; q += blockDim.x) {
     const bool sup = q >= 16 * ns;
     const int s_ = sup ? q - 16 * ns : q >> 4, slot = q & 15;
     const int span = sup ? PX_BLK * PX_BLK : PX_BLK;
     const int bx = sup ? s_ % o.sw : (s_ % o.sw) * PX_BLK + (slot & 3), by = sup ? s_ / o.sw : (s_ / o.sw) * PX_BLK + (slot >> 2);
-    const bool in = sup || (bx < o.bw && by < o.bh);
     const int cx0 = bx * span, cy0 = by * span;
+    float* rec = leaves + 48 * (size_t)q;  // block slots only
+    if (!sup)
+      for (int c = 0; c < 48; ++c) rec[c] = PX_FAR32;
     double lo[3] = {CUDART_INF, CUDART_INF, CUDART_INF}, hi[3] = {-CUDART_INF, -CUDART_INF, -CUDART_INF};
-    int cnt = 0;
-    if (in)
-      for (int y = cy0; y < min(cy0 + span, o.h); ++y)
-        for (int x = cx0; x < min(cx0 + span, o.w); ++x) {
-          const int j = map[y * o.w + x];
-          if (j < 0) continue;
-          ++cnt;
-          double f[3];
-          to_frame(a.frame, P[3 * j], P[3 * j + 1], P[3 * j + 2], f);
+    for (int y = cy0; y < min(cy0 + span, o.h); ++y)
+      for (int x = cx0; x < min(cx0 + span, o.w); ++x) {
+        const int j = map[y * o.w + x];
+        if (j < 0) continue;
+        double f[3];
+        to_frame(a.frame, P[3 * j], P[3 * j + 1], P[3 * j + 2], f);
 #pragma unroll
-          for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], f[d]), hi[d] = fmax(hi[d], f[d]);
+        for (int d = 0; d < 3; ++d) lo[d] = fmin(lo[d], f[d]), hi[d] = fmax(hi[d], f[d]);
+        if (!sup) {
+          const int c = (y - cy0) * PX_BLK + (x - cx0);
+          rec[c] = (float)f[0], rec[16 + c] = (float)f[1], rec[32 + c] = (float)f[2];
         }
+      }
     if (sup) {
       float* o6 = bb + 96 * (size_t)ns + 6 * (size_t)s_;
       box32(lo, hi, o6, o6 + 3, 1);
     } else {
       float* blk = bb + 96 * (size_t)s_;
       box32(lo, hi, blk + slot, blk + 48 + slot, 16);
-      if (in) ls[by * o.bw + bx + 1] = cnt;  // turned into offsets below
     }
-  }
-  if (threadIdx.x == 0) ls[0] = 0;
-  __syncthreads();
-  // inclusive scan of the per-block counts (chunked over the CTA)
-  __shared__ int part[256];
-  const int per = (nb + 255) / 256;
-  const int lo_ = min(nb, (int)threadIdx.x * per), hi_ = min(nb, lo_ + per);
-  int s = 0;
-  for (int q = lo_; q < hi_; ++q) s += ls[q + 1];
-  part[threadIdx.x] = s;
-  __syncthreads();
-  for (int d = 1; d < 256; d <<= 1) {
-    const int v = (int)threadIdx.x >= d ? part[threadIdx.x - d] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
-  }
-  int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
-  for (int q = lo_; q < hi_; ++q) {
-    run += ls[q + 1];
-    ls[q + 1] = run;
-  }
-  __syncthreads();
-  // leaf arrays: the block's points in row-major cell order = ascending local index
-  float4* lp = a.leaf32 + off;
-  for (int q = threadIdx.x; q < nb; q += blockDim.x) {
-    const int cx0 = (q % o.bw) * PX_BLK, cy0 = (q / o.bw) * PX_BLK;
-    int k = ls[q];
-    for (int y = cy0; y < min(cy0 + PX_BLK, o.h); ++y)
-      for (int x = cx0; x < min(cx0 + PX_BLK, o.w); ++x) {
-        const int j = map[y * o.w + x];
-        if (j < 0) continue;
-        double f[3];
-        to_frame(a.frame, P[3 * j], P[3 * j + 1], P[3 * j + 2], f);
-        lp[k++] = make_float4((float)f[0], (float)f[1], (float)f[2], __int_as_float(j));
-      }
   }
 }
 
