@@ -468,6 +468,16 @@ __device__ __forceinline__ float nn_threshold(double best, double err) {
   return __fmul_ru(__fmul_ru(s, s), 1.00000095367431640625f);
 }
 
+// The converse bound: a point whose fp32 squared distance is mm lies at most sqrt(U), U = (sqrt(mm) + 2e)^2 (1 + 2^-20),
+// away in exact arithmetic (the same two-sided rounding bound e), so once such a point is known nothing farther than
+// U can win, and every point within U has an fp32 squared distance <= nn_threshold(U) <= the value returned here:
+// sqrt(U) + 2e <= (sqrt(mm) + 4e)(1 + 2^-21), rounded up throughout.
+__device__ __forceinline__ float nn_threshold_f32(float mm, double err) {
+  const float e2 = __double2float_ru(2.0 * err);
+  const float s = __fmul_ru(__fadd_ru(__fadd_ru(__fsqrt_ru(mm), e2), e2), 1.0000019073486328125f);
+  return __fmul_ru(__fmul_ru(s, s), 1.00000095367431640625f);
+}
+
 __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long toff, int nt, double qx, double qy,
                                           double qz, int prev, double gate2, double& best, int& bj) {
   const double* P = T.points + 3 * toff;
@@ -529,6 +539,28 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
           // phase 1 over the leaf record (16 cells): fp32 squared distances two at a time, survivors into a mask
           const ulonglong2* lr = leaves + 12 * (16 * sbi + q);
           unsigned pmask = 0;
+#ifndef PX_NN_NO_LEAFMIN
+          {
+            float d[16];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const ulonglong2 X = __ldg(lr + g), Y = __ldg(lr + 4 + g), Z = __ldg(lr + 8 + g);
+              upk2(pt_pair_dist2(X.x, Y.x, Z.x, QX, QY, QZ), d[4 * g], d[4 * g + 1]);
+              upk2(pt_pair_dist2(X.y, Y.y, Z.y, QX, QY, QZ), d[4 * g + 2], d[4 * g + 3]);
+            }
+            const float m0 = fminf(fminf(d[0], d[1]), d[2]), m1 = fminf(fminf(d[3], d[4]), d[5]), m2 = fminf(fminf(d[6], d[7]), d[8]);
+            const float m3 = fminf(fminf(d[9], d[10]), d[11]), m4 = fminf(fminf(d[12], d[13]), d[14]);
+            const float mm = fminf(fminf(fminf(m0, m1), m2), fminf(fminf(m3, m4), d[15]));
+            if (mm > thr) continue;  // most opened leaves hold no point within the threshold
+            // the leaf's fp32-closest point is at most U = (sqrt(mm) + 2e)^2 (1 + 2^-20) away in exact arithmetic, so
+            // nothing farther than U can win: tighten the threshold BEFORE the exact evaluations (typically one
+            // survivor -- that point -- instead of every point closer than the seed)
+            thr = fminf(thr, nn_threshold_f32(mm, o.err));
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              if (!(d[k] > thr)) pmask |= 1u << k;
+          }
+#else
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             const ulonglong2 X = __ldg(lr + g), Y = __ldg(lr + 4 + g), Z = __ldg(lr + 8 + g);
@@ -540,6 +572,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
             if (!(d2_ > thr)) pmask |= 4u << (4 * g);
             if (!(d3 > thr)) pmask |= 8u << (4 * g);
           }
+#endif
           // phase 2: exact fp64 evaluation of the few survivors, reference operation order
           if (pmask) {
             const int cell0 = ((sy * PX_BLK + (q >> 2)) * PX_BLK) * o.w + (sx * PX_BLK + (q & 3)) * PX_BLK;
@@ -552,7 +585,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
               const double d2 = dx * dx + dy * dy + dz * dz;
               if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;
             } while (pmask);
-            if (improved) thr = nn_threshold(best, o.err);
+            if (improved) thr = fminf(thr, nn_threshold(best, o.err));
 #ifdef PX_NN_STATS
             n_improved_ += improved;
 #endif
@@ -821,7 +854,7 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a, int split)
 }
 
 #ifndef PX_NN_MINB
-#define PX_NN_MINB 8
+#define PX_NN_MINB 7
 #endif
 // `split` warps share a candidate (its queries dealt round-robin in chunks of 32): small batches do not fill
 // the GPU with one warp per candidate, and the queries are independent.
