@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(128) gicp_solve_kernel(RefineArgs a) {
 __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineArgs a, int it) {
   constexpr int NTMAX = PX_HALVE_NTMAX;
   __shared__ __align__(16) double sm_pose[4][NTMAX][12];
-  __shared__ __align__(16) double sm_term[4][NTMAX][32];
+  __shared__ __align__(16) double sm_term[4][NTMAX][34];  // rows padded: the trials' rows start in different banks
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 4 + wid;
   if (c >= a.src.n) return;
@@ -1214,12 +1214,14 @@ __global__ void __launch_bounds__(128, PX_HALVE_MINB) gicp_halve_kernel(RefineAr
 #pragma unroll
         for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
       }
-      const double2* s2 = reinterpret_cast<const double2*>(sm_term[wid][my]);
+      if (lane < NT) {  // the ordered sum of trial `lane`; only these lanes' sums are read below
+        const double2* s2 = reinterpret_cast<const double2*>(sm_term[wid][lane]);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double2 v = s2[j];
-        f += v.x;
-        f += v.y;
+        for (int j = 0; j < 16; ++j) {
+          const double2 v = s2[j];
+          f += v.x;
+          f += v.y;
+        }
       }
       __syncwarp();
     }
@@ -1521,7 +1523,7 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_ke
   constexpr int NTMAX = PX_HALVE_NTMAX;
   __syncwarp();  // hg has been read by every lane; the staging rows are free
   double(*sm_pose)[12] = reinterpret_cast<double(*)[12]>(stage);              // [NTMAX][12]
-  double(*sm_term)[32] = reinterpret_cast<double(*)[32]>(stage + NTMAX * 12);  // [NTMAX][32]
+  double(*sm_term)[34] = reinterpret_cast<double(*)[34]>(stage + NTMAX * 12);  // [NTMAX][32 + 2]: rows in different banks
   int acc_s = -1, acc_tr = 0;
   double f_acc = 0.0;
   int NT = st[ST_LASTTR] >= PX_HALVE_NT ? NTMAX : PX_HALVE_NT;  // trials in the first pass (a power of two)
@@ -1591,12 +1593,14 @@ __global__ void __launch_bounds__(PX_GICP_WARPS * 32, PX_GICP_MINB) gicp_step_ke
 #pragma unroll
         for (int q = 0; q < 3; ++q) cur[9 + q] = soa[q * plane + si], cur[12 + q] = __ldg(tsoa + q * tplane + tj);
       }
-      const double2* s2 = reinterpret_cast<const double2*>(sm_term[my]);
+      if (lane < NT) {  // the ordered sum of trial `lane`; only these lanes' sums are read below (one wavefront per load)
+        const double2* s2 = reinterpret_cast<const double2*>(sm_term[lane]);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double2 v = s2[j];
-        f += v.x;
-        f += v.y;
+        for (int j = 0; j < 16; ++j) {
+          const double2 v = s2[j];
+          f += v.x;
+          f += v.y;
+        }
       }
       __syncwarp();
     }
