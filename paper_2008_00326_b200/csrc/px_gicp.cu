@@ -461,10 +461,19 @@ __device__ __forceinline__ f32x2 pt_pair_dist2(f32x2 x, f32x2 y, f32x2 z, f32x2 
 // tie the current winner; everything else is evaluated in fp64 with the
 // reference's operation order on the original coordinates.  Results are therefore
 // bit-identical to the linear scan (tests: organised == generic).
-__device__ __forceinline__ float nn_threshold(double best, double err) {
-  // every step rounds towards +inf, so the fp32 result is >= (sqrt(best) + 2 err)^2 (1 + 2^-20) in exact
-  // arithmetic: a looser threshold only lets a few more nodes through to the exact fp64 evaluation
-  const float s = __fadd_ru(__fsqrt_ru(__double2float_ru(best)), __double2float_ru(2.0 * err));
+// Upper bound on sqrt(x): the hardware approximation (MUFU, relative error <= 2^-23 -- PTX ISA, sqrt.approx.f32)
+// times (1 + 2^-22), rounded up.  An IEEE square root with directed rounding is a ~15-instruction software routine,
+// and the thresholds below are recomputed for every leaf that improves the search.
+__device__ __forceinline__ float sqrt_upper(float x) {
+  float s;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(x));
+  return __fmul_ru(s, 1.0000002384185791015625f);
+}
+// e2 = 2 err rounded up (once per query)
+__device__ __forceinline__ float nn_threshold(double best, float e2) {
+  // every step rounds towards +inf (or over-estimates), so the fp32 result is >= (sqrt(best) + 2 err)^2 (1 + 2^-20) in
+  // exact arithmetic: a looser threshold only lets a few more nodes through to the exact fp64 evaluation
+  const float s = __fadd_ru(sqrt_upper(__double2float_ru(best)), e2);
   return __fmul_ru(__fmul_ru(s, s), 1.00000095367431640625f);
 }
 
@@ -472,9 +481,8 @@ __device__ __forceinline__ float nn_threshold(double best, double err) {
 // away in exact arithmetic (the same two-sided rounding bound e), so once such a point is known nothing farther than
 // U can win, and every point within U has an fp32 squared distance <= nn_threshold(U) <= the value returned here:
 // sqrt(U) + 2e <= (sqrt(mm) + 4e)(1 + 2^-21), rounded up throughout.
-__device__ __forceinline__ float nn_threshold_f32(float mm, double err) {
-  const float e2 = __double2float_ru(2.0 * err);
-  const float s = __fmul_ru(__fadd_ru(__fadd_ru(__fsqrt_ru(mm), e2), e2), 1.0000019073486328125f);
+__device__ __forceinline__ float nn_threshold_f32(float mm, float e2) {
+  const float s = __fmul_ru(__fadd_ru(__fadd_ru(sqrt_upper(mm), e2), e2), 1.0000019073486328125f);
   return __fmul_ru(__fmul_ru(s, s), 1.00000095367431640625f);
 }
 
@@ -492,7 +500,8 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
       const double d2 = dx * dx + dy * dy + dz * dz;
       if (d2 <= best) best = d2, bj = prev;
     }
-    float thr = nn_threshold(best, o.err);
+    const float e2 = __double2float_ru(2.0 * o.err);
+    float thr = nn_threshold(best, e2);
 #ifdef PX_NN_STATS
     int n_leaves_ = 0, n_improved_ = 0;
 #endif
@@ -555,7 +564,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
             // the leaf's fp32-closest point is at most U = (sqrt(mm) + 2e)^2 (1 + 2^-20) away in exact arithmetic, so
             // nothing farther than U can win: tighten the threshold BEFORE the exact evaluations (typically one
             // survivor -- that point -- instead of every point closer than the seed)
-            thr = fminf(thr, nn_threshold_f32(mm, o.err));
+            thr = fminf(thr, nn_threshold_f32(mm, e2));
 #pragma unroll
             for (int k = 0; k < 16; ++k)
               if (!(d[k] > thr)) pmask |= 1u << k;
@@ -585,7 +594,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
               const double d2 = dx * dx + dy * dy + dz * dz;
               if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;
             } while (pmask);
-            if (improved) thr = fminf(thr, nn_threshold(best, o.err));
+            if (improved) thr = fminf(thr, nn_threshold(best, e2));
 #ifdef PX_NN_STATS
             n_improved_ += improved;
 #endif
@@ -854,7 +863,7 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a, int split)
 }
 
 #ifndef PX_NN_MINB
-#define PX_NN_MINB 7
+#define PX_NN_MINB 8
 #endif
 // `split` warps share a candidate (its queries dealt round-robin in chunks of 32): small batches do not fill
 // the GPU with one warp per candidate, and the queries are independent.
@@ -876,13 +885,14 @@ __global__ void __launch_bounds__(128, PX_NN_MINB) gicp_nn_kernel(RefineArgs a, 
   const double gate2 = a.cfg.gate2;
   for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
     const double ax = soa[i], ay = soa[plane + i], az = soa[2 * plane + i];
+    const int seed = it == 1 ? -1 : nn[i];
     const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
     const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
     const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
     double best;
     int bj;
     // seed: this point's gated neighbour of the previous iteration (read before it is overwritten)
-    nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, it == 1 ? -1 : nn[i], gate2, best, bj);
+    nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, seed, gate2, best, bj);
     nn[i] = (bj >= 0 && !(best > gate2)) ? bj : -1;  // registration.py:261
 #ifdef PX_NN_STATS
     {
