@@ -872,6 +872,7 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
   const double gate = cfg->max_correspondence_distance;
   if (k < 4 || k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k_covariance out of range [4,32]");
   if (!(gate > 0.0)) return fail(ctx, PX_E_ARG, "max_correspondence_distance must be positive");
+  if (!(gate <= PX_GATE_MAX)) return fail(ctx, PX_E_LIMIT, "max_correspondence_distance above 1e3 m (fp32 pruning thresholds must stay finite)");
   CU(cudaSetDevice(ctx->device));
   const long long total = n_targets ? (long long)offsets[n_targets] : 0;
   for (int i = 0; i < n_targets; ++i)
@@ -1051,6 +1052,8 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
   const int k = cfg->k_covariance;
   if (k < 4 || k > PX_KCOV_MAX) return fail(ctx, PX_E_LIMIT, "k_covariance out of range [4,32]");
   if (!(cfg->max_correspondence_distance > 0.0)) return fail(ctx, PX_E_ARG, "max_correspondence_distance must be positive");
+  if (!(cfg->max_correspondence_distance <= PX_GATE_MAX))
+    return fail(ctx, PX_E_LIMIT, "max_correspondence_distance above 1e3 m (fp32 pruning thresholds must stay finite)");
   if (!ctx->have_scene || !ctx->organised) return fail(ctx, PX_E_ARG, "targets can only be cropped from an organised scene cloud");
   const size_t n1 = (size_t)std::max(n, 1);
   CU(ctx->tgt_sizes.ensure(3 * n1 * 8));

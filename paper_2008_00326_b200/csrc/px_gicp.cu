@@ -453,8 +453,9 @@ __device__ __forceinline__ f32x2 pt_pair_dist2(f32x2 x, f32x2 y, f32x2 z, f32x2 
 // whenever that scan's winner passes the gate; bj = -1 if no point is within the
 // gate.  `prev` (last iteration's correspondence, or -1) seeds the cut-off.
 //
-// Pruning runs in fp32 on conservatively rounded copies (boxes as centre /
-// half-extent, points as float3 + index): with e = T.org.err bounding every
+// Pruning runs in fp32 on conservatively rounded copies (boxes as {lo, hi} rounded
+// outwards, points as fixed 16-cell leaf records of fp32 planes), two boxes / two
+// points per instruction (FADD2 / FMUL2 / FFMA2): with e = T.org.err bounding every
 // rounding involved, a node or point whose fp32 squared distance exceeds
 //     thr = roundup_f32((sqrt(best) + 2e)^2 * (1 + 2^-20))
 // is provably farther than `best` in exact arithmetic, so it can neither beat nor
@@ -590,6 +591,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
               const int k = __ffs(pmask) - 1;
               pmask &= pmask - 1;
               const int j = __ldg(map + cell0 + (k >> 2) * o.w + (k & 3));
+              if (j < 0) continue;  // cannot happen while thr is finite (gate <= PX_GATE_MAX): an absent cell is infinitely far
               const double dx = P[3 * j] - qx, dy = P[3 * j + 1] - qy, dz = P[3 * j + 2] - qz;
               const double d2 = dx * dx + dy * dy + dz * dz;
               if (d2 < best || (d2 == best && j < bj)) best = d2, bj = j, improved = true;

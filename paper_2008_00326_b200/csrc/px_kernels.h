@@ -89,6 +89,7 @@ struct CloudsDev {
 // PX_BLK block of map cells (bh x bw of them) followed by those of every PX_BLK x
 // PX_BLK group of blocks (sh x sw).
 #define PX_BLK 4
+#define PX_GATE_MAX 1e3   // metres: larger gates are refused (PX_E_LIMIT) so that every fp32 pruning threshold stays finite
 #define PX_FAR32 1e30f  // coordinate of an absent leaf point / bound of an empty box: every distance to it overflows to +inf
 struct TgtOrg {
   int gx0, gy0, w, h;

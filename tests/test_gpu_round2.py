@@ -157,6 +157,10 @@ def test_limits_are_errors_not_different_answers(engine):
     with pytest.raises(DeviceError, match="k_covariance"):
         engine.upload_targets(np.array([0, 50]), np.random.default_rng(0).normal(size=(50, 3)),
                               dataclasses.replace(cfg.gicp, k_covariance=33))
+    # a gate so wide that the fp32 pruning thresholds of the NN search could overflow is refused
+    with pytest.raises(DeviceError, match="max_correspondence_distance"):
+        engine.upload_targets(np.array([0, 50]), np.random.default_rng(0).normal(size=(50, 3)),
+                              dataclasses.replace(cfg.gicp, max_correspondence_distance=1e4))
     # stale targets under resident candidates are caught at run time, not read out of bounds
     engine.prepare_plan(frame, models, plan)
     engine.search_upload(plan)
