@@ -433,3 +433,33 @@ def test_device_at_benchmark_density_against_the_reference(engine):
             assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
             wt, wr = G.pose_delta(np.array(a["pose"]).reshape(3, 4), np.array(b["pose"]).reshape(3, 4))
             assert wt <= 1e-4 and wr <= 1e-4
+
+
+@pytest.mark.parametrize("name,gate,jitter", [("c1_box_3dof", 0.01, 0.0), ("c1_box_3dof", 0.2, 0.02),
+                                              ("c4_mixed_6dof", 0.05, 0.01), ("c2_twocyl_color1", 0.03, 0.03)])
+def test_two_wide_nn_search_equals_the_linear_scan(engine, name, gate, jitter):
+    """The box hierarchy / fixed leaf records / two-wide fp32 tests / leaf-minimum threshold of gicp_nn_kernel prune
+    conservatively: refining against ORGANISED targets (hierarchy, in the camera frame for host-built targets) and
+    against the same targets as generic clouds (the reference's linear scan, registration.py:251-261) gives the same
+    bits -- at a tight gate (most queries unmatched), a wide one (every leaf within reach), from perturbed starts
+    (seeded and unseeded queries mixed) and on 6-DoF label targets (many super-blocks, ragged map edges)."""
+    d, frame, models, cfg, plan = G.scene(name)
+    gcfg = dataclasses.replace(cfg.gicp, max_correspondence_distance=gate, max_iterations=6)
+    engine.upload_scene(frame, cfg.stride, plan.observed, plan.obs_labels)
+    engine.upload_models(models)
+    sel = np.arange(0, plan.n, max(1, plan.n // 300))
+    rng = np.random.default_rng(7)
+    inits = np.tile(np.eye(4)[:3], (len(sel), 1, 1))
+    inits[:, :, 3] = rng.normal(scale=jitter, size=(len(sel), 3)) if jitter else 0.0
+    h = engine.render_clouds_handle(plan.flat_oid[sel], plan.cam_poses[sel], cfg.occluder_marking, cfg.delta)
+    try:
+        engine.upload_targets(plan.target_offsets, plan.target_points, gcfg, plan.target_obs_index)
+        To, ito, flo, _, tro, nto = engine.refine_handle(h, plan.target_idx[sel], gcfg, inits, want_trace=True)
+        engine.upload_targets(plan.target_offsets, plan.target_points, gcfg, None)
+        Tg, itg, flg, _, trg, ntg = engine.refine_handle(h, plan.target_idx[sel], gcfg, inits, want_trace=True)
+    finally:
+        engine.lib.px_clouds_free(engine.ctx, h)
+    assert np.array_equal(ito, itg) and np.array_equal(flo, flg) and np.array_equal(nto, ntg)
+    assert np.array_equal(tro, trg)          # the objective of every iteration, bit for bit
+    assert np.array_equal(To, Tg)
+    assert (itg > 0).sum() > len(sel) // 4   # the comparison is not vacuous
