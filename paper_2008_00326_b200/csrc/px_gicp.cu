@@ -528,6 +528,12 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
         // arithmetic, no control flow (slots outside the map hold empty boxes) -- survivors into a bit mask
         const ulonglong2* pl = reinterpret_cast<const ulonglong2*>(bb + 96 * sbi);
         unsigned bmask = 0;
+#ifndef PX_NN_NO_NEAREST_FIRST
+        unsigned kmin = 0xffffffffu;  // (box distance bits, low 4 bits = slot) of the nearest block: non-negative floats order like their bits
+#define PX_KMIN(d, slot) kmin = min(kmin, (__float_as_uint(d) & ~15u) | (unsigned)(slot))
+#else
+#define PX_KMIN(d, slot)
+#endif
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const ulonglong2 lx = __ldg(pl + g), ly = __ldg(pl + 4 + g), lz = __ldg(pl + 8 + g);
@@ -539,11 +545,38 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
           if (!(d1 > thr)) bmask |= 2u << (4 * g);
           if (!(d2_ > thr)) bmask |= 4u << (4 * g);
           if (!(d3 > thr)) bmask |= 8u << (4 * g);
+          PX_KMIN(d0, 4 * g), PX_KMIN(d1, 4 * g + 1), PX_KMIN(d2_, 4 * g + 2), PX_KMIN(d3, 4 * g + 3);
         }
+#undef PX_KMIN
         NN_STAT(3, PX_BLK * PX_BLK);
+#ifndef PX_NN_NO_NEAREST_FIRST
+        // The NEAREST block is opened first -- its leaf usually holds the winner, and the threshold tightened there
+        // closes most of the other blocks that passed the test above: each of those is re-tested (six scalar loads)
+        // against the current threshold before its 192-byte leaf is fetched.  The warp waits for the lane that opens
+        // the most leaves, so this is worth more than the leaves it saves on average.
+        const float thr_blk = thr;  // the threshold the mask was built with
+        bool first = true;
+#endif
         while (bmask) {
+#ifndef PX_NN_NO_NEAREST_FIRST
+          int q;
+          if (first) {
+            q = (int)(kmin & 15u), first = false;  // its bit is set: the mask is not empty and it is the minimum
+          } else {
+            q = __ffs(bmask) - 1;
+          }
+          bmask &= ~(1u << q);
+          if (thr < thr_blk) {
+            const float* bf = bb + 96 * sbi + q;
+            const float gx = fmaxf(fmaxf(__ldg(bf) - qxf, qxf - __ldg(bf + 48)), 0.f);
+            const float gy = fmaxf(fmaxf(__ldg(bf + 16) - qyf, qyf - __ldg(bf + 64)), 0.f);
+            const float gz = fmaxf(fmaxf(__ldg(bf + 32) - qzf, qzf - __ldg(bf + 80)), 0.f);
+            if (fmaf(gz, gz, fmaf(gy, gy, gx * gx)) > thr) continue;
+          }
+#else
           const int q = __ffs(bmask) - 1;
           bmask &= bmask - 1;
+#endif
           NN_STAT(4, 16);
           NN_STAT(6, 1);
           // phase 1 over the leaf record (16 cells): fp32 squared distances two at a time, survivors into a mask
