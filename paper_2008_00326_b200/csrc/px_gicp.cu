@@ -902,9 +902,12 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a, int split)
 #endif
 // `split` warps share a candidate (its queries dealt round-robin in chunks of 32): small batches do not fill
 // the GPU with one warp per candidate, and the queries are independent.
-__global__ void __launch_bounds__(128, PX_NN_MINB) gicp_nn_kernel(RefineArgs a, int it, int split) {
+#ifndef PX_NN_WARPS
+#define PX_NN_WARPS 4  // warps (candidates) per CTA; a CTA's slot is held until its slowest warp is done
+#endif
+__global__ void __launch_bounds__(32 * PX_NN_WARPS, PX_NN_MINB * 4 / PX_NN_WARPS) gicp_nn_kernel(RefineArgs a, int it, int split) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * 4 + wid;
+  const int gw = blockIdx.x * PX_NN_WARPS + wid;
   const int c = gw / split, slice = gw - c * split;
   if (c >= a.src.n) return;
   if (a.st_i[8 * (size_t)c + ST_DONE]) return;
@@ -1800,7 +1803,7 @@ cudaError_t launch_linearize_once(const RefineArgs& a, cudaStream_t st) {
   gicp_init_kernel<<<(unsigned)((a.src.n + 3) / 4), 128, smem_init, st>>>(a, 1);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
-  gicp_nn_kernel<<<(unsigned)((a.src.n + 3) / 4), 128, 0, st>>>(a, 1, 1);
+  gicp_nn_kernel<<<(unsigned)((a.src.n + PX_NN_WARPS - 1) / PX_NN_WARPS), 32 * PX_NN_WARPS, 0, st>>>(a, 1, 1);
   gicp_lin_kernel<<<(a.src.n + PX_GICP_WARPS - 1) / PX_GICP_WARPS, PX_GICP_WARPS * 32, smem, st>>>(a, 1);
   return cudaGetLastError();
 }
@@ -1849,7 +1852,7 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   const int nn_split = (int)std::min<long long>(PX_NN_SPLIT_MAX, std::max<long long>(1, (148LL * 32 * PX_NN_FILL + a.src.n - 1) / a.src.n));
   for (int it = 1; it <= a.cfg.max_iter; ++it) {
     PX_MARK();
-    gicp_nn_kernel<<<(unsigned)(((long long)a.src.n * nn_split + 3) / 4), 128, 0, st>>>(a, it, nn_split);
+    gicp_nn_kernel<<<(unsigned)(((long long)a.src.n * nn_split + PX_NN_WARPS - 1) / PX_NN_WARPS), 32 * PX_NN_WARPS, 0, st>>>(a, it, nn_split);
     PX_MARK();
 #ifdef PX_GICP_SPLIT
     gicp_lin_kernel<<<blocks, PX_GICP_WARPS * 32, smem, st>>>(a, it);
