@@ -418,10 +418,54 @@ def full_fixture(name, frame, models, cfg):
     print(f"[{name}] n={n} -> {(OUT / (name + '.npz')).stat().st_size / 1024:.0f} KiB", flush=True)
 
 
+def full_fixture_6dof(name, frame, models, cfg, pose_every=8):
+    """Same for the 6-DoF workload bench.py --workload c4 measures (BASELINE configs[3], 249,738 mask-constrained
+    candidates): integer costs, GICP iteration counts and first / final render point counts of EVERY candidate (the final
+    count is a function of the refined pose), the refined pose itself (translation + rotation vector, float32) of every
+    `pose_every`-th, and the result JSON."""
+    import dataclasses
+    print(f"[{name}] staged reference run ...", flush=True)
+    st = staged_search(frame, models, cfg)
+    n = len(st["flat"])
+    sel = np.arange(0, n, pose_every)
+    tv = np.empty((sel.size, 6), dtype=np.float32)
+    for q, j in enumerate(sel):
+        p = st["refined"][j]
+        r = p.rotation
+        ang = math.acos(max(-1.0, min(1.0, (np.trace(r) - 1.0) / 2.0)))
+        ax = np.array([r[2, 1] - r[1, 2], r[0, 2] - r[2, 0], r[1, 0] - r[0, 1]])
+        nrm = np.linalg.norm(ax)
+        rv = ax / nrm * ang if nrm > 1e-12 else np.zeros(3)
+        tv[q] = (*p.translation, *rv)
+    d = {"cfg_json": np.array(json.dumps({**cfg.to_dict(), "max_proposals": cfg.max_proposals})),
+         "scene_digest": np.frombuffer(sha(pack_frame(frame)["depth_mm"]), dtype=np.uint8),
+         "pose_every": np.array(pose_every), "pose_tv": tv,
+         "reg_iters": np.array([r.iterations for r in st["regs"]], dtype=np.int8),
+         "n0": np.array([len(c) for c in st["clouds0"]], dtype=np.int16),
+         "n1": np.array([len(c) for c in st["clouds1"]], dtype=np.int16)}
+    del st
+    print(f"[{name}] full reference run with trace ...", flush=True)
+    trace = tempfile.mktemp(suffix=".jsonl")
+    res = rs.estimate_poses(frame, models, dataclasses.replace(cfg, trace_path=trace))
+    rows = [json.loads(line) for line in open(trace)]
+    assert len(rows) == n
+    assert max(r["j_o"] for r in rows) < 32767 and max(r["j_r"] for r in rows) < 32767
+    d["j_o"] = np.array([r["j_o"] for r in rows], dtype=np.int16)
+    d["j_r"] = np.array([r["j_r"] for r in rows], dtype=np.int16)
+    d["result_json"] = np.array(rs.result_to_json(res))
+    np.savez_compressed(OUT / f"{name}.npz", **d)
+    print(f"[{name}] n={n} -> {(OUT / (name + '.npz')).stat().st_size / 1024:.0f} KiB", flush=True)
+
+
 def main():
     OUT.mkdir(parents=True, exist_ok=True)
     which = set(sys.argv[1:]) or {"units", "c1", "c2", "c3", "c3n", "c4", "tiny", "c3d"}
-    if "c3f" in which:  # ~15 minutes on 8 cores: only on request
+    if "c4f" in which:  # ~45 minutes on 8 cores: only on request
+        frame, models = scene_c4()
+        full_fixture_6dof("c4f_full_reference", frame, models,
+                          rs.SearchConfig(mode="6dof", viewpoints=642, n_inplane=36, z_step=0.01, max_proposals=None,
+                                          workers=WORKERS))
+    if "c3f" in which:  # ~5 minutes on 8 cores: only on request
         frame, models = scene_c3()
         full_fixture("c3f_full_reference", frame, models,
                      rs.SearchConfig(mode="3dof", workspace=(-0.32, 0.32, -0.32, 0.32), dt=0.025, workers=WORKERS))

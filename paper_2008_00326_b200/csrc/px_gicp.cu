@@ -880,7 +880,59 @@ __global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a, int split)
 #endif
     double* nd = sm + (size_t)wid * (cfg.k_cov * 48) + lane;
     int* ni = reinterpret_cast<int*>(sm + (size_t)wid * (cfg.k_cov * 48) + cfg.k_cov * 32) + lane;
+#ifndef PX_INIT_NO_CLASSES
+    // Visiting order: a warp waits for its slowest lane, and a point on the silhouette -- half or three quarters of its
+    // rings empty -- searches two to three times as many cells as an interior one.  The points are therefore visited
+    // class by class (5x5 neighbourhood inside the silhouette / at least 15 of its cells / fewer), so that the 32
+    // searches of a step are of one kind.  Results are written by point index: any order gives the same planes.
+    // (With several warps per candidate every warp builds the same spans and the same permutation -- identical
+    // stores, no cross-warp dependence.)  The permutation lives in the nn[] plane, unused before the first NN launch.
+    int32_t* perm = a.nn + v.off;
+    {
+      int2* span = reinterpret_cast<int2*>(G + 3 * plane);  // fourth scratch plane: first / last non-empty cell per grid row
+      for (int y = lane; y < bb.w; y += 32) {
+        int lo = bb.z, hi = -1;
+        for (int x = 0; x < bb.z; ++x)
+          if (map[y * bb.z + x] >= 0) lo = min(lo, x), hi = x;
+        span[y] = make_int2(lo, hi);
+      }
+      __syncwarp();
+      auto classify = [&](int i) {
+        const int cx = spx[2 * i] / stp - bb.x, cy = spx[2 * i + 1] / stp - bb.y;
+        int covered = 0;
+#pragma unroll
+        for (int dy = -2; dy <= 2; ++dy) {
+          const int y = cy + dy;
+          if (y < 0 || y >= bb.w) continue;
+          const int2 sp = span[y];
+          covered += max(0, min(cx + 2, sp.y) - max(cx - 2, sp.x) + 1);
+        }
+        return covered >= 24 ? 0 : (covered >= 15 ? 1 : 2);
+      };
+      int n0 = 0, n1 = 0;
+      for (int base = 0; base < v.n; base += 32) {
+        const int i = base + lane;
+        const int cls = i < v.n ? classify(i) : 3;
+        n0 += __popc(__ballot_sync(0xffffffffu, cls == 0)), n1 += __popc(__ballot_sync(0xffffffffu, cls == 1));
+      }
+      int o0 = 0, o1 = n0, o2 = n0 + n1;
+      for (int base = 0; base < v.n; base += 32) {
+        const int i = base + lane;
+        const int cls = i < v.n ? classify(i) : 3;
+        const unsigned m0 = __ballot_sync(0xffffffffu, cls == 0), m1 = __ballot_sync(0xffffffffu, cls == 1),
+                       m2 = __ballot_sync(0xffffffffu, cls == 2), below = (1u << lane) - 1u;
+        if (cls == 0) perm[o0 + __popc(m0 & below)] = i;
+        if (cls == 1) perm[o1 + __popc(m1 & below)] = i;
+        if (cls == 2) perm[o2 + __popc(m2 & below)] = i;
+        o0 += __popc(m0), o1 += __popc(m1), o2 += __popc(m2);
+      }
+      __syncwarp();
+    }
+    for (int s_ = slice * 32 + lane; s_ < v.n; s_ += 32 * split) {
+      const int i = perm[s_];
+#else
     for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
+#endif
       double cv[12];
       knn_ring_dense<32>(G, plane, map, bb.z, bb.w, src[3 * i], src[3 * i + 1], src[3 * i + 2], spx[2 * i] / stp - bb.x,
                          spx[2 * i + 1] / stp - bb.y, cfg.k_cov, ray_k, nd, ni);
