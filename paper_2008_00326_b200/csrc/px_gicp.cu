@@ -827,7 +827,10 @@ __device__ __forceinline__ void store_src_soa(double* soa, long long plane, int 
 }
 
 // `split` (1, 2 or 4) warps of a CTA share a candidate: small batches do not fill the GPU with one warp each.
-__global__ void __launch_bounds__(128) gicp_init_kernel(RefineArgs a, int split) {
+#ifndef PX_INIT_MINB
+#define PX_INIT_MINB 7  // resident CTAs per SM asked of ptxas: 72 registers; shared memory allows 7 at k = 20 (swept 4..8: 16.3 / 14.3 / 13.2 / 12.7 / 13.5 ms)
+#endif
+__global__ void __launch_bounds__(128, PX_INIT_MINB) gicp_init_kernel(RefineArgs a, int split) {
   extern __shared__ __align__(16) double sm[];  // per warp: [k][32] doubles + [k][32] ints of neighbour lists
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = (blockIdx.x * 4 + wid) / split, slice = wid % split;

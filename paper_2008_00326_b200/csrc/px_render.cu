@@ -147,7 +147,10 @@ __global__ void __launch_bounds__(256) bbox_kernel(RenderArgs a) {
 //   path B: zbits[PX_TILE_PIX] u64, owner[PX_TILE_PIX] i32
 
 template <bool DENSE>
-__global__ void __launch_bounds__(PX_RENDER_THREADS) render_kernel(RenderArgs a) {
+#ifndef PX_RENDER_MINB
+#define PX_RENDER_MINB 8  // 64 registers (swept 3..16: 2.6 / 2.1 / 1.9 / 1.7 / 1.5 / 1.5 / 1.7 / 2.6 ms per launch)
+#endif
+__global__ void __launch_bounds__(PX_RENDER_THREADS, PX_RENDER_MINB) render_kernel(RenderArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int warp_tot[PX_RENDER_THREADS / 32];
   __shared__ int s_base;
