@@ -421,22 +421,30 @@ def full_fixture(name, frame, models, cfg):
 def full_fixture_6dof(name, frame, models, cfg, pose_every=8):
     """Same for the 6-DoF workload bench.py --workload c4 measures (BASELINE configs[3], 249,738 mask-constrained
     candidates): integer costs, GICP iteration counts and first / final render point counts of EVERY candidate (the final
-    count is a function of the refined pose), the refined pose itself (translation + rotation vector, float32) of every
+    count is a function of the refined pose), the refined pose itself (translation + unit quaternion, float32) of every
     `pose_every`-th, and the result JSON."""
     import dataclasses
     print(f"[{name}] staged reference run ...", flush=True)
     st = staged_search(frame, models, cfg)
     n = len(st["flat"])
     sel = np.arange(0, n, pose_every)
-    tv = np.empty((sel.size, 6), dtype=np.float32)
+    tv = np.empty((sel.size, 7), dtype=np.float32)  # translation, unit quaternion (w, x, y, z)
     for q, j in enumerate(sel):
         p = st["refined"][j]
         r = p.rotation
-        ang = math.acos(max(-1.0, min(1.0, (np.trace(r) - 1.0) / 2.0)))
-        ax = np.array([r[2, 1] - r[1, 2], r[0, 2] - r[2, 0], r[1, 0] - r[0, 1]])
-        nrm = np.linalg.norm(ax)
-        rv = ax / nrm * ang if nrm > 1e-12 else np.zeros(3)
-        tv[q] = (*p.translation, *rv)
+        # Shepperd's method: the largest of (trace, r00, r11, r22) picks a well-conditioned branch at every angle
+        c = [r[0, 0] + r[1, 1] + r[2, 2], r[0, 0], r[1, 1], r[2, 2]]
+        b = int(np.argmax(c))
+        if b == 0:
+            qq = [1.0 + c[0], r[2, 1] - r[1, 2], r[0, 2] - r[2, 0], r[1, 0] - r[0, 1]]
+        elif b == 1:
+            qq = [r[2, 1] - r[1, 2], 1.0 + 2 * r[0, 0] - c[0], r[0, 1] + r[1, 0], r[0, 2] + r[2, 0]]
+        elif b == 2:
+            qq = [r[0, 2] - r[2, 0], r[0, 1] + r[1, 0], 1.0 + 2 * r[1, 1] - c[0], r[1, 2] + r[2, 1]]
+        else:
+            qq = [r[1, 0] - r[0, 1], r[0, 2] + r[2, 0], r[1, 2] + r[2, 1], 1.0 + 2 * r[2, 2] - c[0]]
+        qq = np.array(qq) / np.linalg.norm(qq)
+        tv[q] = (*p.translation, *qq)
     d = {"cfg_json": np.array(json.dumps({**cfg.to_dict(), "max_proposals": cfg.max_proposals})),
          "scene_digest": np.frombuffer(sha(pack_frame(frame)["depth_mm"]), dtype=np.uint8),
          "pose_every": np.array(pose_every), "pose_tv": tv,

@@ -320,7 +320,10 @@ __device__ __forceinline__ void store_cov(const CovArgs& a, long long i, const d
 }
 
 // one CTA per target cloud, threads over its points
-__global__ void __launch_bounds__(128) cov_kernel(CovArgs a) {
+#ifndef PX_COV_MINB
+#define PX_COV_MINB 4
+#endif
+__global__ void __launch_bounds__(128, PX_COV_MINB) cov_kernel(CovArgs a) {
   const int c = blockIdx.x;
   const long long off = a.offset[c];
   const int n = a.count ? a.count[c] : (int)(a.offset[c + 1] - off);

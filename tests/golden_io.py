@@ -142,3 +142,33 @@ def compare_with_full_reference(frame, dd, out, index=None):
     bad = set(idx[~(close & same)].tolist())
     iters = set(idx[out.iterations != dd["reg_iters"][idx]].tolist())
     return bad, iters
+
+
+def quat_to_matrix(q):
+    """(n,4) unit quaternions (w, x, y, z) -> (n,3,3) rotations."""
+    q = np.asarray(q, dtype=np.float64)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    return np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)], axis=1),
+                     np.stack([2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)], axis=1),
+                     np.stack([2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)], axis=1)], axis=1)
+
+
+def compare_with_full_reference_6dof(dd, out, index=None):
+    """Run `out` (over candidates `index`, default all 249,738) against tests/golden/c4f_full_reference.npz:
+    (candidates whose integer costs or final-render count differ, candidates among the pose samples whose refined pose
+    is off by more than 1e-4 m / 1e-4 rad, candidates whose iteration count differs).  First-render counts must be equal."""
+    idx = np.arange(len(dd["n0"])) if index is None else np.asarray(index)
+    assert np.array_equal(out.n_first, dd["n0"][idx])
+    same = (out.j_o == dd["j_o"][idx]) & (out.j_r == dd["j_r"][idx]) & (out.n_rendered == dd["n1"][idx])
+    iters = set(idx[out.iterations != dd["reg_iters"][idx]].tolist())
+    pe = int(dd["pose_every"])
+    sel = np.nonzero(idx % pe == 0)[0]
+    ref = dd["pose_tv"][idx[sel] // pe].astype(np.float64)
+    P = out.refined_cam[sel]
+    dt = np.linalg.norm(P[:, :, 3] - ref[:, :3], axis=1)
+    rel = np.einsum("nij,nkj->nik", P[:, :, :3], quat_to_matrix(ref[:, 3:]))
+    dr = np.arccos(np.clip((np.trace(rel, axis1=1, axis2=2) - 1.0) / 2.0, -1.0, 1.0))
+    # the fixture keeps float32: 1e-4 plus its quantisation (6e-8 relative of ~1 m, 1.2e-7 rad)
+    off = (dt > 1e-4 + 5e-7) | (dr > 1e-4 + 5e-7)
+    return set(idx[~same].tolist()), set(idx[sel][off].tolist()), iters
