@@ -172,3 +172,11 @@ def compare_with_full_reference_6dof(dd, out, index=None):
     # the fixture keeps float32: 1e-4 plus its quantisation (6e-8 relative of ~1 m, 1.2e-7 rad)
     off = (dt > 1e-4 + 5e-7) | (dr > 1e-4 + 5e-7)
     return set(idx[~same].tolist()), set(idx[sel][off].tolist()), iters
+
+
+# The 6-DoF benchmark workload (249,738 candidates) against the reference itself: candidates whose integer costs or
+# final-render count differ (10), sampled candidates whose refined pose differs (4 of 31,218; two of them keep their
+# costs), candidates whose iteration count differs -- SURVEY 7.3 H4's chaos again, the same sets for port and device.
+FULL6_CHAOTIC = {73806, 228273, 228544, 229090, 229180, 229270, 230143, 230144, 230323, 230324}
+FULL6_POSE = {228272, 228544, 229000, 230144}
+FULL6_ITERS = {73806, 73986, 228273, 228362, 228363, 228454, 228543, 228544, 229090, 229270}

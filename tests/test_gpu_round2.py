@@ -489,3 +489,26 @@ def test_device_on_the_whole_benchmark_step_against_the_reference(engine):
             assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
             wt, wr = G.pose_delta(np.array(a["pose"]).reshape(3, 4), np.array(b["pose"]).reshape(3, 4))
             assert wt <= 1e-4 and wr <= 1e-4
+
+
+def test_device_on_the_whole_6dof_workload_against_the_reference(engine):
+    """BASELINE configs[3] as bench.py --workload c4 times it -- all 249,738 mask-constrained 6-DoF candidates -- against
+    the REFERENCE ITSELF (tests/golden/c4f_full_reference.npz, oracle/make_golden.py c4f): first-render counts of every
+    candidate; final-render count and both integer costs of all but the 10 named in golden_io.FULL6_CHAOTIC; the refined
+    pose (1e-4 m / 1e-4 rad) of all but 4 of the 31,218 the fixture keeps; iteration counts of all but 10; every winner."""
+    import bench
+    dd = G.load("c4f_full_reference")
+    frame, models, cfg, spec = bench.build_workload("c4", 1, 1, materialise_targets=False)
+    ref_cfg = json.loads(str(dd["cfg_json"]))
+    assert spec.n == 249738 == len(dd["n0"]) and (cfg.viewpoints, cfg.n_inplane, cfg.z_step) == (ref_cfg["viewpoints"], ref_cfg["n_inplane"], ref_cfg["z_step"])
+    out = engine.run_plan(frame, models, spec)
+    bad, badpose, iters = G.compare_with_full_reference_6dof(dd, out)
+    print(f"whole 6-DoF workload: n={spec.n} costs differ {sorted(bad)} poses differ {sorted(badpose)}")
+    assert bad == G.FULL6_CHAOTIC and badpose == G.FULL6_POSE and iters == G.FULL6_ITERS   # pinned to the measured sets
+    ref = json.loads(str(dd["result_json"]))
+    got = json.loads(result_to_json(assemble_result(spec, out, 0.0)))
+    assert got["proposals_evaluated"] == ref["proposals_evaluated"] == 249738
+    for a, b in zip(ref["objects"], got["objects"]):
+        assert (a["proposal_index"], a["j_o"], a["j_r"], a["provenance"]) == (b["proposal_index"], b["j_o"], b["j_r"], b["provenance"])
+        wt, wr = G.pose_delta(np.array(a["pose"]).reshape(3, 4), np.array(b["pose"]).reshape(3, 4))
+        assert wt <= 1e-4 and wr <= 1e-4

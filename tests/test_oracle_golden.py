@@ -277,3 +277,16 @@ def test_oracle_on_the_benchmark_step_against_the_reference():
     print(f"benchmark step, every sixth cell: n={pick.size} divergent {sorted(bad)}")
     assert bad == G.FULL_CHAOTIC & set(pick.tolist())
     assert iters <= G.FULL_CHAOTIC | G.FULL_ITERS_ONLY
+
+
+def test_oracle_on_the_6dof_workload_against_the_reference():
+    """The C port against the reference's outputs on the whole 6-DoF workload (249,738 candidates, tests/golden/
+    c4f_full_reference.npz), here on every 21st candidate (11,893; the GPU test covers all of them)."""
+    import bench
+    dd = G.load("c4f_full_reference")
+    frame, models, cfg, plan = bench.build_workload("c4", 1, 1, materialise_targets=True)
+    pick = np.arange(0, plan.n, 21)
+    out = O.run_plan(frame, models, plan, index=pick, n_threads=8)
+    bad, badpose, iters = G.compare_with_full_reference_6dof(dd, out, pick)
+    here = set(pick.tolist())
+    assert bad == G.FULL6_CHAOTIC & here and badpose <= G.FULL6_POSE and iters == G.FULL6_ITERS & here
