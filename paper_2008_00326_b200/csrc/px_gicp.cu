@@ -535,7 +535,7 @@ __device__ __forceinline__ void nn_target(const TargetsDev& T, int ti, long long
         unsigned kmin = 0xffffffffu;  // (box distance bits, low 4 bits = slot) of the nearest block: non-negative floats order like their bits
 #define PX_KMIN(d, slot) kmin = min(kmin, (__float_as_uint(d) & ~15u) | (unsigned)(slot))
 #else
-#define PX_KMIN(d, slot)
+#define PX_KMIN(d, slot) (void)0
 #endif
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
