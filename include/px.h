@@ -43,12 +43,12 @@ typedef struct px_clouds px_clouds; /* device-resident ragged batch of LabeledCl
 
 /* GicpConfig, registration.py:26-42 */
 typedef struct {
-  int32_t k_covariance;
+  int32_t k_covariance;                /* 4 .. 32, else PX_E_LIMIT */
   int32_t max_iterations;
   double epsilon;
   double translation_tolerance;
   double rotation_tolerance;
-  double max_correspondence_distance;
+  double max_correspondence_distance;  /* metres, (0, 1000]: larger gates are refused with PX_E_LIMIT */
 } px_gicp_cfg;
 
 /* The part of SearchConfig (search.py:37-61) the per-candidate stages read, plus
