@@ -198,10 +198,10 @@ __device__ __forceinline__ void knn_ring(const OrgView& V, int i, int cx, int cy
 // empty) instead of map -> compact index -> point.  The distance comes straight from the cell (one
 // dependent load less per visited cell, NaN fails every comparison); the compact index is only
 // fetched for the cells that enter the list.
-template <int S>
+template <int S, typename IdxT = int>
 __device__ __forceinline__ void knn_ring_dense(const double* __restrict__ G, long long plane, const int32_t* __restrict__ map,
                                                int W, int H, double xi, double yi, double zi, int cx, int cy, int k,
-                                               double ray_k, double* nd, int* ni) {
+                                               double ray_k, double* nd, IdxT* ni) {
   int cnt = 0;
   double worst = CUDART_INF;
   int worst_j = 0x7fffffff;
@@ -225,10 +225,10 @@ __device__ __forceinline__ void knn_ring_dense(const double* __restrict__ G, lon
           pos = k - 1;
         else
           continue;
-        while (pos > 0 && (nd[(pos - 1) * S] > d2 || (nd[(pos - 1) * S] == d2 && ni[(pos - 1) * S] > j)))
+        while (pos > 0 && (nd[(pos - 1) * S] > d2 || (nd[(pos - 1) * S] == d2 && (int)ni[(pos - 1) * S] > j)))
           nd[pos * S] = nd[(pos - 1) * S], ni[pos * S] = ni[(pos - 1) * S], --pos;
-        nd[pos * S] = d2, ni[pos * S] = j;
-        if (cnt == k) worst = nd[(k - 1) * S], worst_j = ni[(k - 1) * S];
+        nd[pos * S] = d2, ni[pos * S] = (IdxT)j;
+        if (cnt == k) worst = nd[(k - 1) * S], worst_j = (int)ni[(k - 1) * S];
       }
     }
     if (cnt == k) {
@@ -240,8 +240,8 @@ __device__ __forceinline__ void knn_ring_dense(const double* __restrict__ G, lon
 
 // mean / covariance / Jacobi / regularised output for a sorted neighbour list
 // (registration.py:143-216)
-template <int S>
-__device__ __forceinline__ void cov_from_neighbours(const double* __restrict__ pts, const int* ni, int k, double eps,
+template <int S, typename IdxT = int>
+__device__ __forceinline__ void cov_from_neighbours(const double* __restrict__ pts, const IdxT* ni, int k, double eps,
                                                     double* __restrict__ out) {
   double mx = 0.0, my = 0.0, mz = 0.0;
   for (int q = 0; q < k; ++q) mx += pts[3 * ni[q * S]], my += pts[3 * ni[q * S] + 1], mz += pts[3 * ni[q * S] + 2];
@@ -830,11 +830,14 @@ __device__ __forceinline__ void store_src_soa(double* soa, long long plane, int 
 }
 
 // `split` (1, 2 or 4) warps of a CTA share a candidate: small batches do not fill the GPU with one warp each.
+#ifndef PX_INIT_U16_MAX
+#define PX_INIT_U16_MAX 0x10000  // clouds up to this many points keep their neighbour indices in 16 bits (0: never, test builds)
+#endif
 #ifndef PX_INIT_MINB
 #define PX_INIT_MINB 7  // resident CTAs per SM asked of ptxas: 72 registers; shared memory allows 7 at k = 20 (swept 4..8: 16.3 / 14.3 / 13.2 / 12.7 / 13.5 ms)
 #endif
 __global__ void __launch_bounds__(128, PX_INIT_MINB) gicp_init_kernel(RefineArgs a, int split) {
-  extern __shared__ __align__(16) double sm[];  // per warp: [k][32] doubles + [k][32] ints of neighbour lists
+  extern __shared__ __align__(16) double sm[];  // per warp: [k][32] doubles + [k][32] 16-bit indices of neighbour lists
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = (blockIdx.x * 4 + wid) / split, slice = wid % split;
   const bool live = c < a.src.n;
@@ -884,8 +887,8 @@ __global__ void __launch_bounds__(128, PX_INIT_MINB) gicp_init_kernel(RefineArgs
 #else
     const double ray_k = window_ray_k(a.cam, bb.x, bb.y, bb.z, bb.w);  // the candidate's screen box
 #endif
-    double* nd = sm + (size_t)wid * (cfg.k_cov * 48) + lane;
-    int* ni = reinterpret_cast<int*>(sm + (size_t)wid * (cfg.k_cov * 48) + cfg.k_cov * 32) + lane;
+    double* nd = sm + (size_t)wid * (cfg.k_cov * 40) + lane;
+    unsigned short* ni = reinterpret_cast<unsigned short*>(sm + (size_t)wid * (cfg.k_cov * 40) + cfg.k_cov * 32) + lane;
 #ifndef PX_INIT_NO_CLASSES
     // Visiting order: a warp waits for its slowest lane, and a point on the silhouette -- half or three quarters of its
     // rings empty -- searches two to three times as many cells as an interior one.  The points are therefore visited
@@ -940,9 +943,17 @@ __global__ void __launch_bounds__(128, PX_INIT_MINB) gicp_init_kernel(RefineArgs
     for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
 #endif
       double cv[12];
-      knn_ring_dense<32>(G, plane, map, bb.z, bb.w, src[3 * i], src[3 * i + 1], src[3 * i + 2], spx[2 * i] / stp - bb.x,
-                         spx[2 * i + 1] / stp - bb.y, cfg.k_cov, ray_k, nd, ni);
-      cov_from_neighbours<32>(src, ni, cfg.k_cov, cfg.eps, cv);
+      if (v.n <= PX_INIT_U16_MAX) {  // neighbour indices fit 16 bits: 80 instead of 96 bytes of list per neighbour slot and lane
+        knn_ring_dense<32, unsigned short>(G, plane, map, bb.z, bb.w, src[3 * i], src[3 * i + 1], src[3 * i + 2],
+                                           spx[2 * i] / stp - bb.x, spx[2 * i + 1] / stp - bb.y, cfg.k_cov, ray_k, nd, ni);
+        cov_from_neighbours<32, unsigned short>(src, ni, cfg.k_cov, cfg.eps, cv);
+      } else {  // a cloud of more than 65,536 points (most of a full-resolution frame): thread-local lists
+        double nd_l[PX_KCOV_MAX];
+        int ni_l[PX_KCOV_MAX];
+        knn_ring_dense<1, int>(G, plane, map, bb.z, bb.w, src[3 * i], src[3 * i + 1], src[3 * i + 2], spx[2 * i] / stp - bb.x,
+                               spx[2 * i + 1] / stp - bb.y, cfg.k_cov, ray_k, nd_l, ni_l);
+        cov_from_neighbours<1, int>(src, ni_l, cfg.k_cov, cfg.eps, cv);
+      }
       store_src_soa(soa, plane, i, src, cv);
     }
   } else {
@@ -1856,7 +1867,7 @@ void dump_nn_stats() {
 cudaError_t launch_linearize_once(const RefineArgs& a, cudaStream_t st) {
   if (a.src.n == 0) return cudaSuccess;
   cudaError_t e;
-  const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
+  const size_t smem_init = sizeof(double) * 40 * (size_t)a.cfg.k_cov * 4;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
   gicp_init_kernel<<<(unsigned)((a.src.n + 3) / 4), 128, smem_init, st>>>(a, 1);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
@@ -1886,7 +1897,7 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   }
 #endif
   const int b4 = (a.src.n + 3) / 4;
-  const size_t smem_init = sizeof(double) * 48 * (size_t)a.cfg.k_cov * 4;
+  const size_t smem_init = sizeof(double) * 40 * (size_t)a.cfg.k_cov * 4;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
   PX_MARK();
   // 1, 2 or 4 warps per candidate: about two waves of 148 SMs x 24 warps when the batch is small
