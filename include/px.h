@@ -103,6 +103,12 @@ int px_scene_upload(px_ctx* ctx, int32_t H, int32_t W, const double* depth, cons
 int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth_grid, const uint8_t* valid_grid,
                           const int32_t* labels_grid, const double* color_grid, const double intr[4], int32_t stride,
                           int64_t* n_obs_out);
+/* Same from the FULL-resolution planes -- depth (H,W) float64, valid (H,W) uint8, labels (H,W) int32, colour (H,W,3)
+ * float64, all C-contiguous: the library samples plane[::stride, ::stride] itself, into pinned staging memory (numpy's
+ * strided copy of the colour plane was two thirds of the scene upload). */
+int px_scene_upload_frame_full(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
+                               const int32_t* labels, const double* color, const double intr[4], int32_t stride,
+                               int64_t* n_obs_out);
 /* The resident observed cloud (any pointer may be NULL): points (n,3), Lab (n,3), source pixels (n,2), labels (n). */
 int px_scene_download_cloud(px_ctx* ctx, double* points, double* lab, int32_t* src_px, int32_t* labels);
 /* ObjectModel (model.py:75-85): mesh with colours already decoded to linear light

@@ -53,6 +53,7 @@ _SIGS = {
     "px_scene_upload": (C.c_int, [vp, C.c_int32, C.c_int32, f64p, u8p, i32p, f64p, C.c_int32,
                                   f64p, f64p, i32p, i32p, C.c_int64]),
     "px_scene_upload_frame": (C.c_int, [vp, C.c_int32, C.c_int32, f64p, u8p, i32p, f64p, f64p, C.c_int32, i64p]),
+    "px_scene_upload_frame_full": (C.c_int, [vp, C.c_int32, C.c_int32, f64p, u8p, i32p, f64p, f64p, C.c_int32, i64p]),
     "px_scene_download_cloud": (C.c_int, [vp, f64p, f64p, i32p, i32p]),
     "px_search_upload_lattice": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(Lattice), f64p, C.c_int32, f64p,
                                            C.POINTER(GicpCfg), C.c_int32, C.c_int32, i64p]),

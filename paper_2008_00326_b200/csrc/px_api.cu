@@ -103,6 +103,8 @@ struct px_ctx {
   DevBuf r_T, r_iters, r_flags, r_pose, r_jo, r_jr, r_nfirst, r_nfinal, r_key, bitmap, r_ncorr, r_cap0, r_cap1, r_nm, r_nfp;
   int bitmap_slots = 0;
   long long* total_host = nullptr;  // pinned
+  void* frame_stage = nullptr;      // pinned staging of the stride-grid samples of a frame (px_scene_upload_frame_full)
+  size_t frame_stage_cap = 0;
   double stage_ms[4] = {0, 0, 0, 0};
   bool kernel_timing = false;           // px_ctx_set_kernel_timing
   std::vector<cudaEvent_t> marks;       // per-launch event marks of the refine stage
@@ -441,6 +443,7 @@ void px_ctx_destroy(px_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t e : ctx->marks) cudaEventDestroy(e);
   if (ctx->total_host) cudaFreeHost(ctx->total_host);
+  if (ctx->frame_stage) cudaFreeHost(ctx->frame_stage);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -593,6 +596,43 @@ int px_scene_upload_frame(px_ctx* ctx, int32_t H, int32_t W, const double* depth
   ctx->bitmap_slots = 0;
   if (n_obs_out) *n_obs_out = n_obs;
   return 0;
+}
+
+int px_scene_upload_frame_full(px_ctx* ctx, int32_t H, int32_t W, const double* depth, const uint8_t* valid,
+                               const int32_t* labels, const double* color, const double intr[4], int32_t stride,
+                               int64_t* n_obs_out) {
+  if (!ctx) return PX_E_ARG;
+  if (H <= 0 || W <= 0 || stride < 1 || !depth || !valid || !labels || !color || !intr)
+    return fail(ctx, PX_E_ARG, "px_scene_upload_frame_full: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  const int GW = (W + stride - 1) / stride, GH = (H + stride - 1) / stride;
+  const size_t ng = (size_t)GW * GH;
+  // one pinned block: depth (8 ng) | colour (24 ng) | labels (4 ng) | valid (ng)
+  const size_t need = ng * 37 + 64;
+  if (ctx->frame_stage_cap < need) {
+    if (ctx->frame_stage) cudaFreeHost(ctx->frame_stage);
+    ctx->frame_stage = nullptr, ctx->frame_stage_cap = 0;
+    CU(cudaMallocHost(&ctx->frame_stage, need));
+    ctx->frame_stage_cap = need;
+  }
+  CU(cudaStreamSynchronize(ctx->stream));  // a previous upload may still be reading the staging block
+  double* sd = static_cast<double*>(ctx->frame_stage);
+  double* sc = sd + ng;
+  int32_t* sl = reinterpret_cast<int32_t*>(sc + 3 * ng);
+  uint8_t* sv = reinterpret_cast<uint8_t*>(sl + ng);
+  for (int gy = 0; gy < GH; ++gy) {
+    const size_t row = (size_t)gy * stride * W;
+    double* od = sd + (size_t)gy * GW;
+    double* oc = sc + 3 * (size_t)gy * GW;
+    int32_t* ol = sl + (size_t)gy * GW;
+    uint8_t* ov = sv + (size_t)gy * GW;
+    for (int gx = 0; gx < GW; ++gx) {
+      const size_t px = row + (size_t)gx * stride;
+      od[gx] = depth[px], ol[gx] = labels[px], ov[gx] = valid[px] ? 1 : 0;
+      oc[3 * gx] = color[3 * px], oc[3 * gx + 1] = color[3 * px + 1], oc[3 * gx + 2] = color[3 * px + 2];
+    }
+  }
+  return px_scene_upload_frame(ctx, H, W, sd, sv, sl, sc, intr, stride, n_obs_out);
 }
 
 int px_scene_download_cloud(px_ctx* ctx, double* points, double* lab, int32_t* src_px, int32_t* labels) {

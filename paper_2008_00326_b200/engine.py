@@ -91,11 +91,27 @@ class Engine:
         self._scene_key = key
         self._keep = [frame]
 
-    def upload_frame(self, frame, stride: int) -> int:
+    def upload_frame(self, frame, stride: int, sample_on_host: bool = False) -> int:
         """Scene upload with the observed cloud built on the device (raster.frame_to_cloud + cloud_labels,
-        raster.py:191-217); returns the number of observed points."""
+        raster.py:191-217); returns the number of observed points.  `sample_on_host` forces the path taken for planes
+        that are not C-contiguous float64 / int32 / bool arrays (numpy samples the stride grid)."""
         k = frame.intrinsics
-        # the batch path reads the frame at the stride-grid pixels only: sample on the host, upload a quarter of the bytes
+        dv, vv, lv, cv = frame.depth.values, frame.depth.valid, frame.labels, frame.color
+        if (not sample_on_host and all(isinstance(a, np.ndarray) and a.flags.c_contiguous for a in (dv, vv, lv, cv)) and dv.dtype == np.float64
+                and cv.dtype == np.float64 and lv.dtype == np.int32 and vv.dtype in (np.bool_, np.uint8)
+                and dv.shape == vv.shape == lv.shape == (k.height, k.width) and cv.shape == (k.height, k.width, 3)):
+            # the library samples the stride grid itself (C loop into pinned memory: numpy's strided copy of the colour
+            # plane alone took longer than the whole upload)
+            intr = np.array([k.fx, k.fy, k.cx, k.cy], dtype=np.float64)
+            n = C.c_int64(0)
+            rc = self.lib.px_scene_upload_frame_full(self.ctx, k.height, k.width, N.ptr(dv, N.f64p), N.ptr(vv.view(np.uint8), N.u8p),
+                                                     N.ptr(lv, N.i32p), N.ptr(cv, N.f64p), N.ptr(intr, N.f64p), int(stride),
+                                                     C.cast(C.byref(n), N.i64p))
+            N.check(self.ctx, rc, "px_scene_upload_frame_full")
+            self._scene_key = None
+            self._keep = [frame]
+            return int(n.value)
+        # other layouts / dtypes: sample on the host, upload a quarter of the bytes
         depth = N.f64(frame.depth.values[::stride, ::stride])
         valid = np.ascontiguousarray(frame.depth.valid[::stride, ::stride], dtype=np.uint8)
         labels = N.i32(frame.labels[::stride, ::stride])

@@ -220,6 +220,14 @@ def test_device_observed_cloud_equals_host(engine, name):
     assert np.array_equal(pts, plan.observed.points) and np.array_equal(src, plan.observed.source_pixel)
     assert np.array_equal(lbl, plan.obs_labels)
     assert np.abs(lab - plan.observed.lab_colors).max() < 1e-9
+    # planes that are not C-contiguous go through host-side sampling (px_scene_upload_frame) instead of the library's own
+    # (px_scene_upload_frame_full): same cloud, bit for bit, also at a stride that does not divide the image
+    for stride in (cfg.stride, 3):
+        n1 = engine.upload_frame(frame, stride)
+        a = engine.download_scene_cloud(n1)
+        n2 = engine.upload_frame(frame, stride, sample_on_host=True)
+        b = engine.download_scene_cloud(n2)
+        assert n1 == n2 and all(np.array_equal(x, y) for x, y in zip(a, b))
 
 
 def _lattice_cfgs():
