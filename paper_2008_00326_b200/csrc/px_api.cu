@@ -254,7 +254,7 @@ CloudsDev clouds_dev(const CloudStore& cs) {
 
 int ensure_bitmap(px_ctx* ctx) {
   const int words = (ctx->cam.GW * ctx->cam.GH + 31) / 32 + 1;
-  const int slots = 148 * 8 * PX_COST_WARPS;
+  const int slots = 148 * 32;  // one wave of persistent warps at 64 registers, whatever the CTA shape (multiple of PX_COST_WARPS)
   const size_t bytes = sizeof(uint32_t) * (size_t)words * slots;
   if (ctx->bitmap.cap < bytes || ctx->bitmap_slots != slots) {
     CU(ctx->bitmap.ensure(bytes));

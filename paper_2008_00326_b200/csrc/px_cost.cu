@@ -42,7 +42,7 @@ __device__ __forceinline__ int warp_max(int v) {
 }
 
 #ifndef PX_COST_MINB
-#define PX_COST_MINB 8  // 64 registers (swept 3..16: 4.0 / 3.5 / 3.3 / 3.2 / 2.4 / 2.9 / 3.3 / 3.5 ms)
+#define PX_COST_MINB (32 / PX_COST_WARPS)  // 64 registers (swept 3..16 CTAs of 4 warps: 4.0 / 3.5 / 3.3 / 3.2 / 2.4 / 2.9 / 3.3 / 3.5 ms)
 #endif
 __global__ void __launch_bounds__(PX_COST_WARPS * 32, PX_COST_MINB) cost_kernel(CostArgs a) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -6,7 +6,9 @@
 
 #include "px_common.cuh"
 
-#define PX_RENDER_THREADS 128
+#ifndef PX_RENDER_THREADS
+#define PX_RENDER_THREADS 64   // swept 32 / 64 / 128 / 256 at 64 registers: 1.40 / 1.43 / 1.50 / 1.74 ms per launch (32 slows the NN kernel's neighbours in the L2)
+#endif
 #define PX_TRI_SMEM 64      // meshes up to this many triangles use the per-pixel path
 #define PX_TILE_PIX 4096    // stride-grid pixels per shared-memory z tile (atomic path)
 #ifndef PX_GICP_WARPS
@@ -15,7 +17,9 @@
 #ifndef PX_GICP_MINB
 #define PX_GICP_MINB 8      // min resident CTAs per SM requested from ptxas (register budget: 128/thread)
 #endif
-#define PX_COST_WARPS 4
+#ifndef PX_COST_WARPS
+#define PX_COST_WARPS 16      // persistent warps per CTA, 148 x 32 of them in all (swept 2 / 4 / 8 / 16: 3.5 / 2.5 / 2.3 / 2.2 ms)
+#endif
 #define PX_KCOV_MAX 32
 
 namespace px {

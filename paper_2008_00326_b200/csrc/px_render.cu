@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) bbox_kernel(RenderArgs a) {
 
 template <bool DENSE>
 #ifndef PX_RENDER_MINB
-#define PX_RENDER_MINB 8  // 64 registers (swept 3..16: 2.6 / 2.1 / 1.9 / 1.7 / 1.5 / 1.5 / 1.7 / 2.6 ms per launch)
+#define PX_RENDER_MINB (1024 / PX_RENDER_THREADS)  // 64 registers (swept 3..16 CTAs of 128 threads: 2.6 / 2.1 / 1.9 / 1.7 / 1.5 / 1.5 / 1.7 / 2.6 ms per launch)
 #endif
 __global__ void __launch_bounds__(PX_RENDER_THREADS, PX_RENDER_MINB) render_kernel(RenderArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
