@@ -833,13 +833,16 @@ __device__ __forceinline__ void store_src_soa(double* soa, long long plane, int 
 #ifndef PX_INIT_U16_MAX
 #define PX_INIT_U16_MAX 0x10000  // clouds up to this many points keep their neighbour indices in 16 bits (0: never, test builds)
 #endif
+#ifndef PX_INIT_WARPS
+#define PX_INIT_WARPS 4  // warps per CTA of gicp_init_kernel (the warps that share a small batch's candidate sit in one CTA)
+#endif
 #ifndef PX_INIT_MINB
 #define PX_INIT_MINB 7  // resident CTAs per SM asked of ptxas: 72 registers; shared memory allows 7 at k = 20 (swept 4..8: 16.3 / 14.3 / 13.2 / 12.7 / 13.5 ms)
 #endif
-__global__ void __launch_bounds__(128, PX_INIT_MINB) gicp_init_kernel(RefineArgs a, int split) {
+__global__ void __launch_bounds__(32 * PX_INIT_WARPS, PX_INIT_MINB) gicp_init_kernel(RefineArgs a, int split) {
   extern __shared__ __align__(16) double sm[];  // per warp: [k][32] doubles + [k][32] 16-bit indices of neighbour lists
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * 4 + wid) / split, slice = wid % split;
+  const int c = (blockIdx.x * PX_INIT_WARPS + wid) / split, slice = wid % split;
   const bool live = c < a.src.n;
   const GicpCfgDev cfg = a.cfg;
   CandView v{};
@@ -1867,9 +1870,9 @@ void dump_nn_stats() {
 cudaError_t launch_linearize_once(const RefineArgs& a, cudaStream_t st) {
   if (a.src.n == 0) return cudaSuccess;
   cudaError_t e;
-  const size_t smem_init = sizeof(double) * 40 * (size_t)a.cfg.k_cov * 4;
+  const size_t smem_init = sizeof(double) * 40 * (size_t)a.cfg.k_cov * PX_INIT_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
-  gicp_init_kernel<<<(unsigned)((a.src.n + 3) / 4), 128, smem_init, st>>>(a, 1);
+  gicp_init_kernel<<<(unsigned)((a.src.n + PX_INIT_WARPS - 1) / PX_INIT_WARPS), 32 * PX_INIT_WARPS, smem_init, st>>>(a, 1);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   gicp_nn_kernel<<<(unsigned)((a.src.n + PX_NN_WARPS - 1) / PX_NN_WARPS), 32 * PX_NN_WARPS, 0, st>>>(a, 1, 1);
@@ -1897,15 +1900,15 @@ cudaError_t launch_refine(const RefineArgs& a, cudaStream_t st, int* launches, c
   }
 #endif
   const int b4 = (a.src.n + 3) / 4;
-  const size_t smem_init = sizeof(double) * 40 * (size_t)a.cfg.k_cov * 4;
+  const size_t smem_init = sizeof(double) * 40 * (size_t)a.cfg.k_cov * PX_INIT_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_init)) != cudaSuccess) return e;
   PX_MARK();
   // 1, 2 or 4 warps per candidate: about two waves of 148 SMs x 24 warps when the batch is small
 #ifndef PX_INIT_SPLIT_N
 #define PX_INIT_SPLIT_N 3552
 #endif
-  const int init_split = a.src.n >= 2 * PX_INIT_SPLIT_N ? 1 : (a.src.n >= PX_INIT_SPLIT_N ? 2 : 4);
-  gicp_init_kernel<<<(unsigned)(((long long)a.src.n * init_split + 3) / 4), 128, smem_init, st>>>(a, init_split);
+  const int init_split = std::min(PX_INIT_WARPS, a.src.n >= 2 * PX_INIT_SPLIT_N ? 1 : (a.src.n >= PX_INIT_SPLIT_N ? 2 : 4));
+  gicp_init_kernel<<<(unsigned)(((long long)a.src.n * init_split + PX_INIT_WARPS - 1) / PX_INIT_WARPS), 32 * PX_INIT_WARPS, smem_init, st>>>(a, init_split);
   const size_t smem = sizeof(double) * WARP_SM_DOUBLES * PX_GICP_WARPS;
   if ((e = cudaFuncSetAttribute(gicp_lin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute(gicp_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
