@@ -1257,6 +1257,12 @@ int px_refine_batch(px_ctx* ctx, const px_clouds* sources, const int32_t* target
       rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
       break;
     }
+    // rows of the objective trace beyond a candidate's accepted steps are never written by the kernels: hand back zeros
+    // (the reference's trace simply ends there), not whatever the allocation held
+    if (out_trace && (e = cudaMemsetAsync(dtr.p, 0, (size_t)n * 16 * (size_t)std::max(cfg->max_iterations, 1), ctx->stream))) {
+      rc = fail(ctx, PX_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
     RefineArgs a{};
     a.src = clouds_dev(sources->s);
     a.tgt = targets_dev(ctx);

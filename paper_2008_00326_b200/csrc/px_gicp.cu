@@ -994,8 +994,9 @@ __global__ void __launch_bounds__(32 * PX_NN_WARPS, PX_NN_MINB * 4 / PX_NN_WARPS
   for (int q = 0; q < 3; ++q) t[q] = a.st_pose[ST_POSE_LD * (size_t)c + 9 + q];
   const double gate2 = a.cfg.gate2;
   for (int i = slice * 32 + lane; i < v.n; i += 32 * split) {
-    const double ax = soa[i], ay = soa[plane + i], az = soa[2 * plane + i];
-    const int seed = it == 1 ? -1 : nn[i];
+    // streamed once per iteration: keep them from displacing the boxes and leaf records in the L1
+    const double ax = PX_LDCS(soa + i), ay = PX_LDCS(soa + plane + i), az = PX_LDCS(soa + 2 * plane + i);
+    const int seed = it == 1 ? -1 : PX_LDCS(nn + i);
     const double px = r[0] * ax + r[1] * ay + r[2] * az + t[0];
     const double py = r[3] * ax + r[4] * ay + r[5] * az + t[1];
     const double pz = r[6] * ax + r[7] * ay + r[8] * az + t[2];
@@ -1003,7 +1004,7 @@ __global__ void __launch_bounds__(32 * PX_NN_WARPS, PX_NN_MINB * 4 / PX_NN_WARPS
     int bj;
     // seed: this point's gated neighbour of the previous iteration (read before it is overwritten)
     nn_target(a.tgt, v.ti, v.toff, v.nt, px, py, pz, seed, gate2, best, bj);
-    nn[i] = (bj >= 0 && !(best > gate2)) ? bj : -1;  // registration.py:261
+    PX_STCS(nn + i, (bj >= 0 && !(best > gate2)) ? bj : -1);  // registration.py:261
 #ifdef PX_NN_STATS
     {
       float* pq = g_nn_prevq + 3 * (v.off + i);
