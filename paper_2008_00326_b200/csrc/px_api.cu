@@ -1073,6 +1073,9 @@ int px_targets_upload(px_ctx* ctx, int32_t n_targets, const int64_t* offsets, co
     CovArgs a{};
     a.n_clouds = n_targets, a.offset = ctx->tgt_off.as<long long>(), a.count = nullptr;
     CU(ctx->tgt_v0.ensure(tot1 * 24));
+    // targets of <= k points get no covariances (registration.py:504-510 skips them): zeros, not stale memory
+    CU(cudaMemsetAsync(ctx->tgt_cov.p, 0, tot1 * 72, ctx->stream));
+    CU(cudaMemsetAsync(ctx->tgt_v0.p, 0, tot1 * 24, ctx->stream));
     a.points = ctx->tgt_pts.as<double>(), a.cov = ctx->tgt_cov.as<double>(), a.v0 = ctx->tgt_v0.as<double>(), a.k = k, a.eps = cfg->epsilon;
     if (org) a.org = ctx->tgt_org.as<TgtOrg>(), a.tmap = ctx->tgt_map.as<int32_t>(), a.tpix = ctx->tgt_pix.as<int32_t>();
     a.ray_k = ctx->cam.ray_k;
@@ -1169,6 +1172,8 @@ static int build_targets_device(px_ctx* ctx, TgtBuildArgs a, const px_gicp_cfg* 
     CU(launch_tgt_fill(a, ctx->stream));
     CovArgs c{};
     c.n_clouds = n, c.offset = off, c.count = nullptr;
+    CU(cudaMemsetAsync(ctx->tgt_cov.p, 0, tot1 * 72, ctx->stream));  // targets of <= k points get none: zeros, not stale memory
+    CU(cudaMemsetAsync(ctx->tgt_v0.p, 0, tot1 * 24, ctx->stream));
     c.points = a.tgt_pts, c.cov = ctx->tgt_cov.as<double>(), c.v0 = ctx->tgt_v0.as<double>(), c.k = k, c.eps = cfg->epsilon;
     c.org = a.org, c.tmap = a.tmap, c.tpix = a.tpix, c.ray_k = ctx->cam.ray_k, c.cam = ctx->cam;
     CU(launch_cov(c, total, ctx->stream));
